@@ -226,6 +226,7 @@ Cls classify(const Grid& g, const double v[3]) {
     double th = std::atan2(rho, v[2]);
     double ph = std::atan2(v[1], v[0]);
     if (ph < 0.0) ph += 2.0 * PI;
+    if (v[0] == 0.0 && v[1] == 0.0) ph = 0.0;  // poles: phi := 0 (reading R7)
     c.us = 2.0 * (c.s - c.is * g.ds) / g.ds - 1.0;
     c.ut = 2.0 * (th - c.it * g.dth) / g.dth - 1.0;
     c.up = 2.0 * (ph - c.ip * g.dth) / g.dth - 1.0;

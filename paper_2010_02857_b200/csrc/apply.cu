@@ -1,0 +1,413 @@
+// apply.cu -- one IFGF operator application (Algorithm 1):
+//   K3 near field, K4 leaf source-to-cone,
+//   K5 Chebyshev coefficient fit,
+//   K6 cousin-point interpolation,
+//   K7 upward interpolation + recentering.
+// Every output has exactly one writer (target-major K3/K6, parent-node-major
+// K7): no atomics on values, deterministic results.
+#include <cmath>
+
+#include "ifgf_internal.cuh"
+
+namespace ifgf {
+
+namespace {
+
+constexpr int TPB = 128;
+constexpr double kInv4Pi = 0.079577471545947667884;  // 1/(4 pi)
+
+inline int nblk(int64_t n, int tpb = TPB) {
+    int64_t b = (n + tpb - 1) / tpb;
+    return (int)(b < 1 ? 1 : b);
+}
+
+__global__ void k_permute(const double2* __restrict__ in, const int* __restrict__ perm, int64_t n, double2* out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[perm[i]];
+}
+__global__ void k_unpermute(const double2* __restrict__ in, const int* __restrict__ perm, int64_t n, double2* out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[perm[i]] = in[i];
+}
+
+// K3: out[l] = sum over owned neighbour boxes B of the leaf T containing l,
+// sum_{m in B, m != l} a_m e^{ik r}/(4 pi r)  (raw kernel, reading R11).
+// One warp per (leaf, 32 targets); sources are read as warp-uniform broadcasts.
+__global__ void __launch_bounds__(TPB) k_near(LevelParams L, const double* __restrict__ px,
+                                              const double* __restrict__ py, const double* __restrict__ pz,
+                                              const double2* __restrict__ a, double k, double2* out) {
+    int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (item >= L.nwitems) return;
+    int2 it = L.witems[item];
+    int T = it.x, l = it.y + lane;
+    if (l >= L.box_start[T + 1]) return;
+    const double x = px[l], y = py[l], z = pz[l];
+    double ar = 0.0, ai = 0.0;
+    for (int e = L.nbr_off[T]; e < L.nbr_off[T + 1]; ++e) {
+        int B = L.nbr_idx[e];
+        if (B < L.b0 || B >= L.b1) continue;
+        int m1 = L.box_start[B + 1];
+        for (int m = L.box_start[B]; m < m1; ++m) {
+            if (m == l) continue;
+            double dx = x - px[m], dy = y - py[m], dz = z - pz[m];
+            double r = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
+            double s, c;
+            sincos(k * r, &s, &c);
+            double w = kInv4Pi / r;
+            double2 am = a[m];
+            double gr = c * w, gi = s * w;
+            ar = fma(am.x, gr, fma(-am.y, gi, ar));
+            ai = fma(am.x, gi, fma(am.y, gr, ai));
+        }
+    }
+    out[l] = make_double2(ar, ai);
+}
+
+__device__ __forceinline__ void node_off(const LevelParams& LP, int Ps, int Pa, int cell, int n, double off[3]) {
+    int is = cell % LP.ns;
+    int ith = (cell / LP.ns) % LP.nC;
+    int iph = cell / (LP.ns * LP.nC);
+    int ks = n % Ps, kt = (n / Ps) % Pa, kp = n / (Ps * Pa);
+    double r = __ldg(LP.rtab + is * Ps + ks);
+    double st = __ldg(LP.st_tab + ith * Pa + kt), ct = __ldg(LP.ct_tab + ith * Pa + kt);
+    double sp = __ldg(LP.sp_tab + iph * Pa + kp), cp = __ldg(LP.cp_tab + iph * Pa + kp);
+    double rs = __dmul_rn(r, st);
+    off[0] = __dmul_rn(rs, cp);
+    off[1] = __dmul_rn(rs, sp);
+    off[2] = __dmul_rn(r, ct);
+}
+
+// K4: V[B, gamma, y] = sum_{m in B} a_m (|y-c|/|y-x_m|) e^{ik(|y-x_m| - |y-c|)}
+// (eq. factored_f P:432-434 at the nodes of eq. interp_pts), block per owned leaf.
+constexpr int S2C_CHUNK = 256;
+__global__ void __launch_bounds__(TPB) k_s2c(LevelParams L, const double* __restrict__ px,
+                                             const double* __restrict__ py, const double* __restrict__ pz,
+                                             const double2* __restrict__ a, double k, int Ps, int Pa,
+                                             double2* vals) {
+    const int P = Ps * Pa * Pa;
+    int64_t B = L.b0 + blockIdx.x;
+    __shared__ double sw[S2C_CHUNK][3];
+    __shared__ double2 sa[S2C_CHUNK];
+    const int64_t row = (B - L.b0) * L.W;
+    const int64_t s0 = L.rank[row], s1 = L.rank[row + L.W];
+    const int64_t nitem = (s1 - s0) * P;
+    if (nitem == 0) return;
+    const double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
+                 cz = box_centre(L, L.box_ijk[3 * B + 2], 2);
+    const int m0 = L.box_start[B], m1 = L.box_start[B + 1];
+    for (int64_t base = 0; base < nitem; base += blockDim.x) {
+        int64_t j = base + threadIdx.x;
+        bool active = j < nitem;
+        double off[3] = {0, 0, 0};
+        int64_t s = 0;
+        int n = 0;
+        if (active) {
+            s = s0 + j / P;
+            n = (int)(j % P);
+            node_off(L, Ps, Pa, L.seg_cell[s], n, off);
+        }
+        const double oo = off[0] * off[0] + off[1] * off[1] + off[2] * off[2];
+        const double ro = sqrt(oo);
+        double vr = 0.0, vi = 0.0;
+        for (int c0 = m0; c0 < m1; c0 += S2C_CHUNK) {
+            int cn = min(S2C_CHUNK, m1 - c0);
+            __syncthreads();
+            for (int t = threadIdx.x; t < cn; t += blockDim.x) {
+                sw[t][0] = px[c0 + t] - cx;
+                sw[t][1] = py[c0 + t] - cy;
+                sw[t][2] = pz[c0 + t] - cz;
+                sa[t] = a[c0 + t];
+            }
+            __syncthreads();
+            if (active) {
+                for (int t = 0; t < cn; ++t) {
+                    double wx = sw[t][0], wy = sw[t][1], wz = sw[t][2];
+                    double dx = off[0] - wx, dy = off[1] - wy, dz = off[2] - wz;
+                    double rd = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
+                    // |y - x_m| - |y - c| = (w.w - 2 off.w) / (|off - w| + |off|)   (reading R17)
+                    double num = fma(wx, wx, fma(wy, wy, wz * wz)) - 2.0 * fma(off[0], wx, fma(off[1], wy, off[2] * wz));
+                    double diff = num / (rd + ro);
+                    double ratio = ro / rd;
+                    double sn, cs;
+                    sincos(k * diff, &sn, &cs);
+                    double gr = ratio * cs, gi = ratio * sn;
+                    double2 am = sa[t];
+                    vr = fma(am.x, gr, fma(-am.y, gi, vr));
+                    vi = fma(am.x, gi, fma(am.y, gr, vi));
+                }
+            }
+        }
+        if (active) vals[s * P + n] = make_double2(vr, vi);
+    }
+}
+
+// K5: node values -> tensor Chebyshev coefficients in place (reading R1),
+// separable passes along s, theta, phi; one warp per segment.
+__global__ void k_fit(int64_t nseg, int Ps, int Pa, const double* __restrict__ Ms, const double* __restrict__ Ma,
+                      double2* vals) {
+    extern __shared__ double2 sm[];
+    const int P = Ps * Pa * Pa;
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (s >= nseg) return;
+    double2* b0 = sm + (size_t)warp * 2 * P;
+    double2* b1 = b0 + P;
+    double2* g = vals + s * P;
+    for (int i = lane; i < P; i += 32) b0[i] = g[i];
+    __syncwarp();
+    for (int i = lane; i < P; i += 32) {  // along s
+        int a = i % Ps, rest = i / Ps;
+        double xr = 0, xi = 0;
+        for (int q = 0; q < Ps; ++q) {
+            double m = __ldg(Ms + a * Ps + q);
+            double2 v = b0[rest * Ps + q];
+            xr = fma(m, v.x, xr);
+            xi = fma(m, v.y, xi);
+        }
+        b1[i] = make_double2(xr, xi);
+    }
+    __syncwarp();
+    for (int i = lane; i < P; i += 32) {  // along theta
+        int a = i % Ps, b = (i / Ps) % Pa, c = i / (Ps * Pa);
+        double xr = 0, xi = 0;
+        for (int q = 0; q < Pa; ++q) {
+            double m = __ldg(Ma + b * Pa + q);
+            double2 v = b1[(c * Pa + q) * Ps + a];
+            xr = fma(m, v.x, xr);
+            xi = fma(m, v.y, xi);
+        }
+        b0[i] = make_double2(xr, xi);
+    }
+    __syncwarp();
+    for (int i = lane; i < P; i += 32) {  // along phi
+        int ab = i % (Ps * Pa), c = i / (Ps * Pa);
+        double xr = 0, xi = 0;
+        for (int q = 0; q < Pa; ++q) {
+            double m = __ldg(Ma + c * Pa + q);
+            double2 v = b0[q * Ps * Pa + ab];
+            xr = fma(m, v.x, xr);
+            xi = fma(m, v.y, xi);
+        }
+        g[i] = make_double2(xr, xi);
+    }
+}
+
+template <int PS, int PA>
+__device__ __forceinline__ double2 interp(const double2* C, int Ps, int Pa, double us, double ut, double up) {
+    if constexpr (PS > 0) {
+        return eval_interp<PS, PA>(C, us, ut, up);
+    } else {
+        return eval_interp_rt(C, Ps, Pa, us, ut, up);
+    }
+}
+
+// K6: I(x) += G(x, c_B) Interp_{B, gamma(x)} F_B(x) for every owned source box B
+// of which x is a cousin point.  Target-major: one warp per
+// (target box T, 32 targets); the cousin relation is symmetric.
+template <int PS, int PA>
+__global__ void __launch_bounds__(TPB) k_cousin(LevelParams L, const double* __restrict__ px,
+                                                const double* __restrict__ py, const double* __restrict__ pz,
+                                                const double2* __restrict__ vals, double k, int Ps, int Pa,
+                                                double2* out, int* bad) {
+    const int P = Ps * Pa * Pa;
+    int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (item >= L.nwitems) return;
+    int2 it = L.witems[item];
+    int T = it.x, l = it.y + lane;
+    if (l >= L.box_start[T + 1]) return;
+    const double x = px[l], y = py[l], z = pz[l];
+    double ar = 0.0, ai = 0.0;
+    for (int e = L.cou_off[T]; e < L.cou_off[T + 1]; ++e) {
+        int B = L.cou_idx[e];
+        if (B < L.b0 || B >= L.b1) continue;
+        double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
+               cz = box_centre(L, L.box_ijk[3 * B + 2], 2);
+        Cls c = classify(L, __dsub_rn(x, cx), __dsub_rn(y, cy), __dsub_rn(z, cz));
+        int64_t slot = seg_slot(L, B, cell_of(L, c));
+        if (slot < 0) {
+            atomicOr(bad, 1);
+            continue;
+        }
+        double2 F = interp<PS, PA>(vals + slot * P, Ps, Pa, c.us, c.ut, c.up);
+        double sn, cs;
+        sincos(k * c.r, &sn, &cs);
+        double w = kInv4Pi / c.r;
+        double gr = cs * w, gi = sn * w;
+        ar = fma(gr, F.x, fma(-gi, F.y, ar));
+        ai = fma(gr, F.y, fma(gi, F.x, ai));
+    }
+    double2 o = out[l];
+    out[l] = make_double2(o.x + ar, o.y + ai);
+}
+
+// K7: V_Q[gamma', y] = sum over owned children B of Q of
+//   Interp_{B, gamma(y)} F_B(y) * G(y, c_B)/G(y, c_Q)
+// one thread per (parent segment, node); y - c_B = off + delta, delta = +-H_d/2.
+template <int PS, int PA>
+__global__ void __launch_bounds__(TPB) k_upward(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
+                                                double k, int Ps, int Pa, double2* vals_p, int* bad) {
+    const int P = Ps * Pa * Pa;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= LP.nseg * P) return;
+    int64_t sp = t / P;
+    int n = (int)(t - sp * P);
+    int Q = LP.seg_box[sp];
+    double off[3];
+    node_off(LP, Ps, Pa, LP.seg_cell[sp], n, off);
+    const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
+    const double hh = 0.5 * L.H;
+    double ar = 0.0, ai = 0.0;
+    for (int B = LP.child_start[Q]; B < LP.child_start[Q + 1]; ++B) {
+        if (B < L.b0 || B >= L.b1) continue;
+        double dx = (L.box_ijk[3 * B] & 1) ? -hh : hh, dy = (L.box_ijk[3 * B + 1] & 1) ? -hh : hh,
+               dz = (L.box_ijk[3 * B + 2] & 1) ? -hh : hh;
+        Cls c = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+        int64_t slot = seg_slot(L, B, cell_of(L, c));
+        if (slot < 0) {
+            atomicOr(bad, 1);
+            continue;
+        }
+        double2 F = interp<PS, PA>(vals_d + slot * P, Ps, Pa, c.us, c.ut, c.up);
+        // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
+        double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
+        double diff = num / (c.r + rQ);
+        double ratio = rQ / c.r;
+        double sn, cs;
+        sincos(k * diff, &sn, &cs);
+        double gr = ratio * cs, gi = ratio * sn;
+        ar = fma(gr, F.x, fma(-gi, F.y, ar));
+        ai = fma(gr, F.y, fma(gi, F.x, ai));
+    }
+    vals_p[sp * P + n] = make_double2(ar, ai);
+}
+
+// ------------------------------------------------------------- dispatch
+template <int PS, int PA>
+struct Kern {
+    static void cousin(dim3 g, cudaStream_t st, const LevelParams& L, const ifgf_plan_s* p, const double2* v,
+                       double2* out, int* bad) {
+        k_cousin<PS, PA><<<g, TPB, 0, st>>>(L, p->px, p->py, p->pz, v, p->k, p->Ps, p->Pa, out, bad);
+    }
+    static void upward(dim3 g, cudaStream_t st, const LevelParams& L, const LevelParams& LP, const ifgf_plan_s* p,
+                       const double2* vd, double2* vp, int* bad) {
+        k_upward<PS, PA><<<g, TPB, 0, st>>>(L, LP, vd, p->k, p->Ps, p->Pa, vp, bad);
+    }
+};
+
+template <class F3, class F5, class FG>
+void dispatch(int Ps, int Pa, F3 f35, F5 f55, FG fg) {
+    if (Ps == 3 && Pa == 5) f35();
+    else if (Ps == 5 && Pa == 5) f55();
+    else fg();
+}
+
+struct Prof {  // CUDA events around each launch (ifgf_profile_enable)
+    ifgf_plan_s* p;
+    cudaStream_t st;
+    int cls = 0;
+    cudaEvent_t e0 = nullptr;
+    Prof(ifgf_plan_s* p_, cudaStream_t s, int c) : p(p_), st(s), cls(c) {
+        if (!p->profile) return;
+        e0 = take();
+        IFGF_CUDA(cudaEventRecord(e0, st));
+    }
+    cudaEvent_t take() {
+        cudaEvent_t e;
+        if (!p->ev_pool.empty()) {
+            e = p->ev_pool.back();
+            p->ev_pool.pop_back();
+        } else {
+            IFGF_CUDA(cudaEventCreate(&e));
+        }
+        return e;
+    }
+    void done() {
+        IFGF_CUDA(cudaGetLastError());
+        if (!p->profile) return;
+        cudaEvent_t e1 = take();
+        IFGF_CUDA(cudaEventRecord(e1, st));
+        p->pending.push_back({cls, e0, e1});
+    }
+};
+
+}  // namespace
+
+void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t st) {
+    const int D = p->D, P = p->P, Ps = p->Ps, Pa = p->Pa;
+    const int64_t n = p->n;
+    const unsigned mask = p->stage_mask;
+    {
+        Prof pr(p, st, 0);
+        k_permute<<<nblk(n, 256), 256, 0, st>>>(dens, p->perm, n, p->a_sorted);
+        pr.done();
+    }
+    LevelHost& LD = p->lev[D];
+    if (mask & IFGF_STAGE_NEAR) {
+        Prof pr(p, st, 1);
+        k_near<<<nblk(LD.p.nwitems * 32), TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, p->out_sorted);
+        pr.done();
+    } else {
+        IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));
+    }
+    bool have = false;  // level d holds coefficients
+    if (D >= 3 && (mask & (IFGF_STAGE_COUSIN | IFGF_STAGE_UPWARD)) && LD.p.b1 > LD.p.b0) {
+        if (LD.p.nseg > 0) {
+            Prof pr(p, st, 2);
+            k_s2c<<<(int)(LD.p.b1 - LD.p.b0), TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa,
+                                                             p->vals[D & 1]);
+            pr.done();
+        }
+        have = true;
+    }
+    const int fit_warps = std::max(1, std::min(4, (int)(48 * 1024 / (32 * P))));
+    const size_t fit_smem = (size_t)fit_warps * 2 * P * sizeof(double2);
+    if (fit_smem > 48 * 1024)
+        IFGF_CUDA(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fit_smem));
+    auto fit = [&](int d) {
+        LevelParams& L = p->lev[d].p;
+        if (L.nseg == 0) return;
+        Prof pr(p, st, 3);
+        k_fit<<<(int)((L.nseg + fit_warps - 1) / fit_warps), 32 * fit_warps, fit_smem, st>>>(
+            L.nseg, Ps, Pa, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]);
+        pr.done();
+    };
+    if (have) fit(D);
+    for (int d = D; d >= 3 && have; --d) {
+        LevelParams& L = p->lev[d].p;
+        const double2* vd = p->vals[d & 1];
+        if ((mask & IFGF_STAGE_COUSIN) && L.nseg > 0 && L.nwitems > 0) {
+            Prof pr(p, st, 4);
+            dim3 g(nblk(L.nwitems * 32));
+            dispatch(
+                Ps, Pa, [&] { Kern<3, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
+                [&] { Kern<5, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
+                [&] { Kern<0, 0>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); });
+            pr.done();
+        }
+        if (d > 3 && (mask & IFGF_STAGE_UPWARD)) {
+            LevelParams& LP = p->lev[d - 1].p;
+            if (LP.nseg > 0) {
+                Prof pr(p, st, 5);
+                dim3 g(nblk(LP.nseg * P));
+                double2* vp = p->vals[(d - 1) & 1];
+                dispatch(
+                    Ps, Pa, [&] { Kern<3, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
+                    [&] { Kern<5, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
+                    [&] { Kern<0, 0>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); });
+                pr.done();
+                fit(d - 1);
+            }
+        } else {
+            have = false;
+        }
+    }
+    {
+        Prof pr(p, st, 6);
+        k_unpermute<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->perm, n, out);
+        pr.done();
+    }
+}
+
+}  // namespace ifgf

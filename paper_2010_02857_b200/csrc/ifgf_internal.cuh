@@ -1,0 +1,324 @@
+// ifgf_internal.cuh -- plan layout, device math and shared helpers of libifgf.
+// Citations P:n are lines of /root/reference/PAPER.md.  Nothing here is shared
+// with oracle/ (the oracle implements the same written contract independently,
+// DESIGN.md "Classification contract").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ifgf.h"
+
+namespace ifgf {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr int kMaxP1 = 16;  // max P_s, P_ang
+
+// ---------------------------------------------------------------------------
+// Error plumbing (host)
+// ---------------------------------------------------------------------------
+struct Error {
+    ifgf_status st;
+    std::string msg;
+};
+void set_error(const std::string& msg);
+#define IFGF_CUDA(call)                                                                              \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess) {                                                                     \
+            throw ::ifgf::Error{e_ == cudaErrorMemoryAllocation ? IFGF_ENOMEM : IFGF_ECUDA,         \
+                                std::string(#call) + ": " + cudaGetErrorString(e_)};                 \
+        }                                                                                            \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Level data: box tree + cone grid + relevant segments of one level d.
+// Boxes are in Morton order; each box owns a contiguous range of the sorted
+// points.  Segment s of the level is (seg_box[s], seg_cell[s]) in (box, cell)
+// order; its P coefficients live at vals[s * P].
+// ---------------------------------------------------------------------------
+struct LevelParams {  // passed by value to kernels
+    int d;
+    int ns, nC;
+    int64_t ncell;       // 2 * ns * nC^2
+    int64_t W;           // 64-bit bitmap words per box
+    double H, h, ds, dth, x0[3];
+    int64_t nbox;
+    int64_t b0, b1;      // owned box range [b0, b1) (source partition)
+    // boxes
+    const int* box_ijk;       // 3 per box
+    const int* box_start;     // nbox + 1 (sorted point ranges)
+    const int* box_parent;    // nbox
+    const int* child_start;   // nbox + 1 (boxes of level d + 1)
+    const int* nbr_off;       // nbox + 1
+    const int* nbr_idx;
+    const int* cou_off;       // nbox + 1
+    const int* cou_idx;
+    // relevant segments (owned boxes only; bitmap rows indexed by b - b0)
+    const unsigned long long* bitmap;
+    const unsigned* rank;     // exclusive prefix popcount over all words (global)
+    int64_t nseg;
+    const int* seg_box;
+    const int* seg_cell;
+    // classification boundary tables (host libm)
+    const double* cos_tb;     // nC + 1
+    const double* cphi;       // 2 nC + 1
+    const double* sphi;       // 2 nC + 1
+    // node geometry tables (host libm): h/s_k, sin/cos theta_i, sin/cos phi_j
+    const double* rtab;       // ns * Ps
+    const double* st_tab;     // nC * Pa
+    const double* ct_tab;
+    const double* sp_tab;     // 2 nC * Pa
+    const double* cp_tab;
+    // K6 warp work items (box, first point)
+    const int2* witems;
+    int64_t nwitems;
+};
+
+struct LevelHost {
+    LevelParams p{};
+    // owned device allocations
+    int *box_ijk = nullptr, *box_start = nullptr, *box_parent = nullptr, *child_start = nullptr;
+    int *nbr_off = nullptr, *nbr_idx = nullptr, *cou_off = nullptr, *cou_idx = nullptr;
+    unsigned long long* bitmap = nullptr;
+    unsigned* rank = nullptr;
+    int *seg_box = nullptr, *seg_cell = nullptr;
+    double *cos_tb = nullptr, *cphi = nullptr, *sphi = nullptr;
+    double *rtab = nullptr, *st_tab = nullptr, *ct_tab = nullptr, *sp_tab = nullptr, *cp_tab = nullptr;
+    int2* witems = nullptr;
+    int64_t ncou = 0, nnbr = 0;
+    std::vector<int> box_ijk_host;  // kept for plan export (small levels only)
+};
+
+}  // namespace ifgf
+
+struct ifgf_plan_s {
+    int device = 0;
+    int64_t n = 0;
+    double k = 0;
+    int D = 1, Ps = 3, Pa = 5, P = 75;
+    unsigned stage_mask = IFGF_STAGE_ALL;
+    int rank = 0, nranks = 1;
+    double root_c[3] = {0, 0, 0}, H1 = 1, x0[3] = {0, 0, 0};
+    std::vector<ifgf::LevelHost> lev;  // 1..D
+    // sorted points (SoA), permutation sorted -> caller
+    double *px = nullptr, *py = nullptr, *pz = nullptr;
+    int* perm = nullptr;
+    // Chebyshev tables
+    double* cheb_Ms = nullptr;  // Ps x Ps fit matrix (2 - delta_i0)/n T_i(t_k)
+    double* cheb_Ma = nullptr;  // Pa x Pa
+    // apply scratch
+    double2* a_sorted = nullptr;
+    double2* out_sorted = nullptr;
+    double2* vals[2] = {nullptr, nullptr};  // ping-pong by level parity
+    int64_t vals_cap[2] = {0, 0};
+    double2* host_stage_dev_in = nullptr;   // ifgf_apply_host buffers
+    double2* host_stage_dev_out = nullptr;
+    // stats / profiling
+    ifgf_stats stats{};
+    bool sticky_cuda_error = false;
+    int profile = 0;
+    double prof_ms[IFGF_NUM_KCLASS] = {0};
+    int64_t prof_launches[IFGF_NUM_KCLASS] = {0};
+    std::vector<cudaEvent_t> ev_pool;
+    struct PendingEv {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<PendingEv> pending;
+    int* dev_bad = nullptr;  // device flag: apply-time invariant violation (EINTERNAL)
+    int64_t device_bytes = 0;
+    std::vector<void*> allocs;  // every cudaMalloc of the plan
+};
+
+namespace ifgf {
+
+// Allocation helper that records ownership in the plan.
+template <class T>
+T* dev_alloc(ifgf_plan_s* p, int64_t count) {
+    if (count <= 0) count = 1;
+    void* ptr = nullptr;
+    IFGF_CUDA(cudaMalloc(&ptr, sizeof(T) * (size_t)count));
+    p->allocs.push_back(ptr);
+    p->device_bytes += (int64_t)(sizeof(T) * (size_t)count);
+    return static_cast<T*>(ptr);
+}
+void dev_free(ifgf_plan_s* p, void* ptr);
+
+void build_plan(ifgf_plan_s* p, const double* points_dev, const ifgf_opts& o);
+void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+struct Cls {
+    int is, it, ip;
+    double r, us, ut, up;
+};
+
+// Classification of the relative vector v at a level (DESIGN.md
+// "Classification contract", reading R7).  The
+// discrete decisions use only IEEE-rounded + - * / sqrt without contraction
+// (explicit __d*_rn) against host-libm boundary tables; atan2 only supplies
+// the first guess and the local coordinates.
+__device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double vy, double vz) {
+    Cls c;
+    double r2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+    c.r = __dsqrt_rn(r2);
+    double s = __ddiv_rn(L.h, c.r);
+    int is = (int)floor(__ddiv_rn(s, L.ds));
+    c.is = is > L.ns - 1 ? L.ns - 1 : is;
+    // theta: i_theta = #{k in 1..nC-1 : vz/r <= cos(k dtheta)}
+    double ct = __ddiv_rn(vz, c.r);
+    double rho = __dsqrt_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)));
+    double th = atan2(rho, vz);
+    int it = (int)(th / L.dth);
+    it = it < 0 ? 0 : (it > L.nC - 1 ? L.nC - 1 : it);
+    while (it > 0 && !(ct <= __ldg(L.cos_tb + it))) --it;
+    while (it < L.nC - 1 && ct <= __ldg(L.cos_tb + it + 1)) ++it;
+    c.it = it;
+    // phi: unique j with cross_j >= 0 > cross_{j+1}; poles -> 0
+    const int n2 = 2 * L.nC;
+    double ph = 0.0;
+    int ip = 0;
+    if (!(vx == 0.0 && vy == 0.0)) {
+        ph = atan2(vy, vx);
+        if (ph < 0.0) ph += 2.0 * kPi;
+        ip = (int)(ph / L.dth);
+        ip = ip < 0 ? 0 : (ip > n2 - 1 ? n2 - 1 : ip);
+        for (int iter = 0; iter < 2 * n2; ++iter) {
+            double cj = __dsub_rn(__dmul_rn(vy, __ldg(L.cphi + ip)), __dmul_rn(vx, __ldg(L.sphi + ip)));
+            if (!(cj >= 0.0)) {
+                ip = ip == 0 ? n2 - 1 : ip - 1;
+                continue;
+            }
+            double cj1 = __dsub_rn(__dmul_rn(vy, __ldg(L.cphi + ip + 1)), __dmul_rn(vx, __ldg(L.sphi + ip + 1)));
+            if (cj1 >= 0.0) {
+                ip = ip == n2 - 1 ? 0 : ip + 1;
+                continue;
+            }
+            break;
+        }
+    }
+    c.ip = ip;
+    c.us = 2.0 * (s - c.is * L.ds) / L.ds - 1.0;
+    c.ut = 2.0 * (th - c.it * L.dth) / L.dth - 1.0;
+    c.up = 2.0 * (ph - c.ip * L.dth) / L.dth - 1.0;
+    return c;
+}
+
+__device__ __forceinline__ int64_t cell_of(const LevelParams& L, const Cls& c) {
+    return ((int64_t)c.ip * L.nC + c.it) * L.ns + c.is;
+}
+
+// Slot of (box b, cell) among the level's relevant segments (O(1) rank lookup),
+// or -1 if the segment is not relevant.
+__device__ __forceinline__ int64_t seg_slot(const LevelParams& L, int64_t b, int64_t cell) {
+    int64_t w = (b - L.b0) * L.W + (cell >> 6);
+    unsigned long long word = __ldg(L.bitmap + w);
+    unsigned long long bit = 1ull << (cell & 63);
+    if (!(word & bit)) return -1;
+    return (int64_t)__ldg(L.rank + w) + __popcll(word & (bit - 1));
+}
+
+__device__ __forceinline__ double box_centre(const LevelParams& L, int k, int axis) {
+    return __dadd_rn(L.x0[axis], __dmul_rn((double)k + 0.5, L.H));
+}
+
+// Chebyshev polynomials T_0..T_{n-1} at u (three-term recurrence).
+template <int N>
+__device__ __forceinline__ void cheb_T(double u, double* T) {
+    T[0] = 1.0;
+    if (N > 1) T[1] = u;
+    const double u2 = 2.0 * u;
+#pragma unroll
+    for (int i = 2; i < N; ++i) T[i] = fma(u2, T[i - 1], -T[i - 2]);
+}
+__device__ __forceinline__ void cheb_T_rt(int n, double u, double* T) {
+    T[0] = 1.0;
+    if (n > 1) T[1] = u;
+    const double u2 = 2.0 * u;
+    for (int i = 2; i < n; ++i) T[i] = fma(u2, T[i - 1], -T[i - 2]);
+}
+
+// Evaluate the tensor Chebyshev interpolant with coefficients C (layout
+// ((c * PA + b) * PS + a) for s-index a, theta-index b, phi-index c) at local
+// coordinates (us, ut, up): contraction over phi, then theta, then s.
+template <int PS, int PA>
+__device__ __forceinline__ double2 eval_interp(const double2* __restrict__ C, double us, double ut, double up) {
+    double Ts[PS], Tt[PA], Tp[PA];
+    cheb_T<PS>(us, Ts);
+    cheb_T<PA>(ut, Tt);
+    cheb_T<PA>(up, Tp);
+    double wr[PA * PS], wi[PA * PS];
+#pragma unroll
+    for (int i = 0; i < PA * PS; ++i) {
+        double2 v = __ldg(C + i);
+        wr[i] = v.x;
+        wi[i] = v.y;
+    }
+#pragma unroll
+    for (int c = 1; c < PA; ++c) {
+#pragma unroll
+        for (int i = 0; i < PA * PS; ++i) {
+            double2 v = __ldg(C + c * PA * PS + i);
+            wr[i] = fma(Tp[c], v.x, wr[i]);
+            wi[i] = fma(Tp[c], v.y, wi[i]);
+        }
+    }
+    double xr[PS], xi[PS];
+#pragma unroll
+    for (int a = 0; a < PS; ++a) {
+        xr[a] = wr[a];
+        xi[a] = wi[a];
+    }
+#pragma unroll
+    for (int b = 1; b < PA; ++b)
+#pragma unroll
+        for (int a = 0; a < PS; ++a) {
+            xr[a] = fma(Tt[b], wr[b * PS + a], xr[a]);
+            xi[a] = fma(Tt[b], wi[b * PS + a], xi[a]);
+        }
+    double fr = xr[0], fi = xi[0];
+#pragma unroll
+    for (int a = 1; a < PS; ++a) {
+        fr = fma(Ts[a], xr[a], fr);
+        fi = fma(Ts[a], xi[a], fi);
+    }
+    return make_double2(fr, fi);
+}
+
+// Runtime-order fallback (any P_s, P_ang <= kMaxP1).
+__device__ __forceinline__ double2 eval_interp_rt(const double2* __restrict__ C, int PS, int PA, double us, double ut,
+                                                  double up) {
+    double Ts[kMaxP1], Tt[kMaxP1], Tp[kMaxP1];
+    cheb_T_rt(PS, us, Ts);
+    cheb_T_rt(PA, ut, Tt);
+    cheb_T_rt(PA, up, Tp);
+    double fr = 0.0, fi = 0.0;
+    for (int c = 0; c < PA; ++c) {
+        double gr = 0.0, gi = 0.0;
+        for (int b = 0; b < PA; ++b) {
+            double hr = 0.0, hi = 0.0;
+            for (int a = 0; a < PS; ++a) {
+                double2 v = __ldg(C + (c * PA + b) * PS + a);
+                hr = fma(Ts[a], v.x, hr);
+                hi = fma(Ts[a], v.y, hi);
+            }
+            gr = fma(Tt[b], hr, gr);
+            gi = fma(Tt[b], hi, gi);
+        }
+        fr = fma(Tp[c], gr, fr);
+        fi = fma(Tp[c], gi, fi);
+    }
+    return make_double2(fr, fi);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+}  // namespace ifgf

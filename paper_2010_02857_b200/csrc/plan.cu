@@ -1,0 +1,836 @@
+// plan.cu -- GPU plan build (T_pre of the paper): Morton-sorted box octree,
+// neighbour / cousin lists, cone grids and the relevant cone segments of
+// every level (eq. defallrelevantconesegments).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "ifgf_internal.cuh"
+
+namespace ifgf {
+
+namespace {
+
+constexpr int TPB = 256;
+
+inline int nblocks(int64_t n, int tpb = TPB) {
+    int64_t b = (n + tpb - 1) / tpb;
+    if (b < 1) b = 1;
+    if (b > 2147483647) b = 2147483647;
+    return (int)b;
+}
+
+// ---------------------------------------------------------------- validation
+__global__ void k_minmax(const double* __restrict__ pts, int64_t n, double* part, int* bad) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    int nonfinite = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        for (int a = 0; a < 3; ++a) {
+            double v = pts[3 * i + a];
+            if (!isfinite(v)) nonfinite = 1;
+            lo[a] = fmin(lo[a], v);
+            hi[a] = fmax(hi[a], v);
+        }
+    }
+    __shared__ double s[6][TPB];
+    for (int a = 0; a < 3; ++a) {
+        s[a][threadIdx.x] = lo[a];
+        s[3 + a][threadIdx.x] = hi[a];
+    }
+    if (nonfinite) atomicOr(bad, 1);
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w)
+            for (int a = 0; a < 3; ++a) {
+                s[a][threadIdx.x] = fmin(s[a][threadIdx.x], s[a][threadIdx.x + w]);
+                s[3 + a][threadIdx.x] = fmax(s[3 + a][threadIdx.x], s[3 + a][threadIdx.x + w]);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int a = 0; a < 6; ++a) part[6 * blockIdx.x + a] = s[a][0];
+}
+
+// --------------------------------------------------------------- Morton keys
+__device__ __forceinline__ uint64_t spread3(uint64_t v) {  // bit b -> bit 3b
+    uint64_t r = 0;
+    for (int b = 0; b < 21; ++b) r |= ((v >> b) & 1ull) << (3 * b);
+    return r;
+}
+__device__ __forceinline__ int compact3(uint64_t v) {
+    int r = 0;
+    for (int b = 0; b < 21; ++b) r |= (int)((v >> (3 * b)) & 1ull) << b;
+    return r;
+}
+__device__ __forceinline__ uint64_t morton(int qx, int qy, int qz) {
+    return (spread3((uint64_t)qx) << 2) | (spread3((uint64_t)qy) << 1) | spread3((uint64_t)qz);
+}
+
+// Leaf coordinates q = clamp(floor((x - x0)/H_D)) (contract) and keys.
+__global__ void k_keys(const double* __restrict__ pts, int64_t n, double x0x, double x0y, double x0z, double HD,
+                       int nmax, uint64_t* keys, int* idx) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double x0[3] = {x0x, x0y, x0z};
+    int q[3];
+    for (int a = 0; a < 3; ++a) {
+        double t = floor(__ddiv_rn(__dsub_rn(pts[3 * i + a], x0[a]), HD));
+        q[a] = t < 0.0 ? 0 : (t >= (double)nmax ? nmax - 1 : (int)t);
+    }
+    keys[i] = morton(q[0], q[1], q[2]);
+    idx[i] = (int)i;
+}
+
+__global__ void k_gather_points(const double* __restrict__ pts, const int* __restrict__ perm, int64_t n, double* px,
+                                double* py, double* pz) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t j = perm[i];
+    px[i] = pts[3 * j];
+    py[i] = pts[3 * j + 1];
+    pz[i] = pts[3 * j + 2];
+}
+
+// ------------------------------------------------------------- box building
+__global__ void k_flag_runs(const uint64_t* __restrict__ key, int64_t n, int shift, int* flag) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    flag[i] = (i == 0 || (key[i] >> shift) != (key[i - 1] >> shift)) ? 1 : 0;
+}
+
+// Leaf level: box index per point from the inclusive scan; box start and key.
+__global__ void k_leaf_boxes(const uint64_t* __restrict__ key, const int* __restrict__ flag,
+                             const int* __restrict__ incl, int64_t n, int* box_start, uint64_t* box_key) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (flag[i]) {
+        int b = incl[i] - 1;
+        box_start[b] = (int)i;
+        box_key[b] = key[i];
+    }
+}
+
+// Coarser level d-1 from level d boxes.
+__global__ void k_parent_boxes(const uint64_t* __restrict__ key_d, const int* __restrict__ start_d,
+                               const int* __restrict__ flag, const int* __restrict__ incl, int64_t nb, int* parent_d,
+                               int* start_p, uint64_t* key_p, int* child_start_p) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    int q = incl[b] - 1;
+    parent_d[b] = q;
+    if (flag[b]) {
+        start_p[q] = start_d[b];
+        key_p[q] = key_d[b] >> 3;
+        child_start_p[q] = (int)b;
+    }
+}
+
+__global__ void k_box_ijk(const uint64_t* __restrict__ key, int64_t nb, int* ijk) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    uint64_t k = key[b];
+    ijk[3 * b] = compact3(k >> 2);
+    ijk[3 * b + 1] = compact3(k >> 1);
+    ijk[3 * b + 2] = compact3(k);
+}
+
+// Pairwise-different points: coincident points share a leaf.
+__global__ void k_coincident(const double* __restrict__ px, const double* __restrict__ py,
+                             const double* __restrict__ pz, const int* __restrict__ start, int64_t nb, int* bad) {
+    int64_t b = blockIdx.x;
+    if (b >= nb) return;
+    int s0 = start[b], s1 = start[b + 1];
+    for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x)
+        for (int j = i + 1; j < s1; ++j)
+            if (px[i] == px[j] && py[i] == py[j] && pz[i] == pz[j]) atomicOr(bad, 1);
+}
+
+__device__ __forceinline__ int64_t find_key(const uint64_t* __restrict__ keys, int64_t nb, uint64_t k) {
+    int64_t lo = 0, hi = nb;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    return (lo < nb && keys[lo] == k) ? lo : -1;
+}
+
+// Neighbours N B: relevant boxes with ||a - k||_inf <= 1, B included.
+// pass 0: count into cnt[b]; pass 1: fill idx from off[b].
+__global__ void k_neighbours(const uint64_t* __restrict__ keys, const int* __restrict__ ijk, int64_t nb, int nside,
+                             int pass, int* cnt, const int* __restrict__ off, int* idx) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    int i0 = ijk[3 * b], j0 = ijk[3 * b + 1], k0 = ijk[3 * b + 2];
+    int c = 0;
+    int64_t o = pass ? off[b] : 0;
+    for (int di = -1; di <= 1; ++di)
+        for (int dj = -1; dj <= 1; ++dj)
+            for (int dk = -1; dk <= 1; ++dk) {
+                int i = i0 + di, j = j0 + dj, k = k0 + dk;
+                if (i < 0 || j < 0 || k < 0 || i >= nside || j >= nside || k >= nside) continue;
+                int64_t a = find_key(keys, nb, morton(i, j, k));
+                if (a < 0) continue;
+                if (pass) idx[o + c] = (int)a;
+                ++c;
+            }
+    if (!pass) cnt[b] = c;
+}
+
+// Cousins M B = (R_B^d \ N B) cap Q N P B (eq. defcousinboxes).
+__global__ void k_cousins(const int* __restrict__ ijk, const int* __restrict__ parent, int64_t nb,
+                          const int* __restrict__ pnbr_off, const int* __restrict__ pnbr_idx,
+                          const int* __restrict__ pchild_start, int pass, int* cnt, const int* __restrict__ off,
+                          int* idx) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    int i0 = ijk[3 * b], j0 = ijk[3 * b + 1], k0 = ijk[3 * b + 2];
+    int P = parent[b];
+    int c = 0;
+    int64_t o = pass ? off[b] : 0;
+    for (int e = pnbr_off[P]; e < pnbr_off[P + 1]; ++e) {
+        int A = pnbr_idx[e];
+        for (int ch = pchild_start[A]; ch < pchild_start[A + 1]; ++ch) {
+            int dist = max(abs(ijk[3 * ch] - i0), max(abs(ijk[3 * ch + 1] - j0), abs(ijk[3 * ch + 2] - k0)));
+            if (dist < 2) continue;
+            if (pass) idx[o + c] = ch;
+            ++c;
+        }
+    }
+    if (!pass) cnt[b] = c;
+}
+
+// Warp work items: (box, first point) chunks of 32 points.
+__global__ void k_witem_count(const int* __restrict__ start, int64_t nb, int* cnt) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    cnt[b] = (start[b + 1] - start[b] + 31) / 32;
+}
+__global__ void k_witem_fill(const int* __restrict__ start, int64_t nb, const int* __restrict__ off, int2* items) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    int o = off[b];
+    for (int p = start[b]; p < start[b + 1]; p += 32) items[o++] = make_int2((int)b, p);
+}
+
+// --------------------------------------------------------- relevance flags
+__device__ __forceinline__ void set_bit(unsigned long long* bm, int64_t w, unsigned long long bit) {
+    if (!(bm[w] & bit)) atomicOr(bm + w, bit);
+}
+
+// (i) cousin surface points: target-major over warp
+// items of level d; every (point x in T, cousin B of T) classifies x - c_B.
+__global__ void k_flag_cousin_points(LevelParams L, const double* __restrict__ px, const double* __restrict__ py,
+                                     const double* __restrict__ pz, unsigned long long* bm, int* bad) {
+    int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (item >= L.nwitems) return;
+    int2 it = L.witems[item];
+    int T = it.x, l = it.y + lane;
+    if (l >= L.box_start[T + 1]) return;
+    double x = px[l], y = py[l], z = pz[l];
+    for (int e = L.cou_off[T]; e < L.cou_off[T + 1]; ++e) {
+        int B = L.cou_idx[e];
+        if (B < L.b0 || B >= L.b1) continue;
+        double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
+               cz = box_centre(L, L.box_ijk[3 * B + 2], 2);
+        Cls c = classify(L, __dsub_rn(x, cx), __dsub_rn(y, cy), __dsub_rn(z, cz));
+        int64_t cell = cell_of(L, c);
+        if (cell < 0 || cell >= L.ncell) { atomicOr(bad, 1); continue; }
+        set_bit(bm, (B - L.b0) * L.W + (cell >> 6), 1ull << (cell & 63));
+    }
+}
+
+// Node offset of node n = (kp*Pa + kt)*Ps + ks of cell `cell` at level LP
+// (eq. interp_pts): r = h/s_k, (r sin th cos ph, r sin th sin ph, r cos th).
+__device__ __forceinline__ void node_offset(const LevelParams& LP, int Ps, int Pa, int cell, int n, double off[3],
+                                            double* r_out) {
+    int is = cell % LP.ns;
+    int ith = (cell / LP.ns) % LP.nC;
+    int iph = cell / (LP.ns * LP.nC);
+    int ks = n % Ps, kt = (n / Ps) % Pa, kp = n / (Ps * Pa);
+    double r = __ldg(LP.rtab + is * Ps + ks);
+    double st = __ldg(LP.st_tab + ith * Pa + kt), ct = __ldg(LP.ct_tab + ith * Pa + kt);
+    double sp = __ldg(LP.sp_tab + iph * Pa + kp), cp = __ldg(LP.cp_tab + iph * Pa + kp);
+    double rs = __dmul_rn(r, st);
+    off[0] = __dmul_rn(rs, cp);
+    off[1] = __dmul_rn(rs, sp);
+    off[2] = __dmul_rn(r, ct);
+    if (r_out) *r_out = r;
+}
+
+// (ii) nodes of relevant parent segments: thread per
+// (parent segment, node); each owned child B of Q classifies off + delta.
+__global__ void k_flag_parent_nodes(LevelParams L, LevelParams LP, int Ps, int Pa, unsigned long long* bm,
+                                    int* bad) {
+    const int P = Ps * Pa * Pa;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= LP.nseg * P) return;
+    int64_t s = t / P;
+    int n = (int)(t - s * P);
+    int Q = LP.seg_box[s];
+    double off[3];
+    node_offset(LP, Ps, Pa, LP.seg_cell[s], n, off, nullptr);
+    const double hh = 0.5 * L.H;  // exact
+    for (int B = LP.child_start[Q]; B < LP.child_start[Q + 1]; ++B) {
+        if (B < L.b0 || B >= L.b1) continue;
+        double dx = (L.box_ijk[3 * B] & 1) ? -hh : hh, dy = (L.box_ijk[3 * B + 1] & 1) ? -hh : hh,
+               dz = (L.box_ijk[3 * B + 2] & 1) ? -hh : hh;
+        Cls c = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+        int64_t cell = cell_of(L, c);
+        if (cell < 0 || cell >= L.ncell) { atomicOr(bad, 1); continue; }
+        set_bit(bm, (B - L.b0) * L.W + (cell >> 6), 1ull << (cell & 63));
+    }
+}
+
+__global__ void k_popc(const unsigned long long* __restrict__ bm, int64_t nw, unsigned* out) {
+    int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (w >= nw) return;
+    out[w] = (unsigned)__popcll(bm[w]);
+}
+
+__global__ void k_emit_segments(const unsigned long long* __restrict__ bm, const unsigned* __restrict__ rank,
+                                int64_t nw, int64_t W, int64_t b0, int* seg_box, int* seg_cell) {
+    int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (w >= nw) return;
+    unsigned long long v = bm[w];
+    if (!v) return;
+    int64_t idx = rank[w];
+    int b = (int)(b0 + w / W);
+    int base = (int)((w % W) * 64);
+    while (v) {
+        int bit = __ffsll((long long)v) - 1;
+        seg_box[idx] = b;
+        seg_cell[idx] = base + bit;
+        ++idx;
+        v &= v - 1;
+    }
+}
+
+// ---------------------------------------------------------------- stats
+__global__ void k_stat_near(LevelParams L, unsigned long long* acc) {
+    int64_t T = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (T >= L.nbox) return;
+    int64_t nT = L.box_start[T + 1] - L.box_start[T], s = 0;
+    for (int e = L.nbr_off[T]; e < L.nbr_off[T + 1]; ++e) {
+        int B = L.nbr_idx[e];
+        if (B < L.b0 || B >= L.b1) continue;
+        s += L.box_start[B + 1] - L.box_start[B];
+    }
+    int64_t own = (T >= L.b0 && T < L.b1) ? nT : 0;  // self pairs excluded
+    atomicAdd(acc, (unsigned long long)(nT * s - own));
+}
+__global__ void k_stat_cousin(LevelParams L, unsigned long long* acc) {
+    int64_t T = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (T >= L.nbox) return;
+    int64_t nT = L.box_start[T + 1] - L.box_start[T], c = 0;
+    for (int e = L.cou_off[T]; e < L.cou_off[T + 1]; ++e) {
+        int B = L.cou_idx[e];
+        if (B >= L.b0 && B < L.b1) ++c;
+    }
+    atomicAdd(acc, (unsigned long long)(nT * c));
+}
+__global__ void k_stat_s2c(LevelParams L, int P, unsigned long long* acc) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= L.nseg) return;
+    int B = L.seg_box[s];
+    atomicAdd(acc, (unsigned long long)((int64_t)P * (L.box_start[B + 1] - L.box_start[B])));
+}
+__global__ void k_stat_up(LevelParams L, LevelParams LP, int P, unsigned long long* acc) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= LP.nseg) return;
+    int Q = LP.seg_box[s];
+    int64_t c = 0;
+    for (int B = LP.child_start[Q]; B < LP.child_start[Q + 1]; ++B)
+        if (B >= L.b0 && B < L.b1) ++c;
+    atomicAdd(acc, (unsigned long long)(c * P));
+}
+
+// ------------------------------------------------------------ host helpers
+struct Scratch {  // temporary device buffers freed at the end of the plan build
+    std::vector<void*> ptrs;
+    template <class T>
+    T* get(int64_t n) {
+        if (n <= 0) n = 1;
+        void* p = nullptr;
+        IFGF_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)n));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    void release(void* p) {
+        for (auto& q : ptrs)
+            if (q == p) {
+                cudaFree(q);
+                q = nullptr;
+            }
+    }
+    ~Scratch() {
+        for (void* p : ptrs)
+            if (p) cudaFree(p);
+    }
+};
+
+template <class T>
+void inclusive_scan(Scratch& S, const T* in, T* out, int64_t n, cudaStream_t st) {
+    size_t bytes = 0;
+    IFGF_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, (int)n, st));
+    void* tmp = S.get<char>((int64_t)bytes);
+    IFGF_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out, (int)n, st));
+    S.release(tmp);
+}
+template <class T>
+void exclusive_scan(Scratch& S, const T* in, T* out, int64_t n, cudaStream_t st) {
+    size_t bytes = 0;
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, st));
+    void* tmp = S.get<char>((int64_t)bytes);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int)n, st));
+    S.release(tmp);
+}
+
+template <class T>
+T d2h_one(const T* p, cudaStream_t st) {
+    T v;
+    IFGF_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, st));
+    IFGF_CUDA(cudaStreamSynchronize(st));
+    return v;
+}
+
+// CSR build from a count kernel: off = exclusive scan of counts (+ total).
+int* csr_offsets(ifgf_plan_s* p, Scratch& S, const int* cnt, int64_t n, cudaStream_t st, int64_t* total) {
+    int* off = dev_alloc<int>(p, n + 1);
+    int* incl = S.get<int>(n);
+    inclusive_scan(S, cnt, incl, n, st);
+    IFGF_CUDA(cudaMemsetAsync(off, 0, sizeof(int), st));
+    IFGF_CUDA(cudaMemcpyAsync(off + 1, incl, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+    *total = d2h_one(off + n, st);
+    S.release(incl);
+    return off;
+}
+
+template <class T>
+T* upload(ifgf_plan_s* p, const std::vector<T>& v, cudaStream_t st) {
+    T* d = dev_alloc<T>(p, (int64_t)v.size());
+    IFGF_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+    IFGF_CUDA(cudaStreamSynchronize(st));
+    return d;
+}
+
+std::vector<double> cheb_nodes(int n) {
+    std::vector<double> t(n);
+    for (int k = 0; k < n; ++k) t[k] = std::cos((2.0 * k + 1.0) * kPi / (2.0 * n));
+    return t;
+}
+
+// Fit matrix M[i][k] = ((2 - delta_i0)/n) T_i(t_k)  (reading R1).
+std::vector<double> cheb_fit_matrix(int n) {
+    std::vector<double> t = cheb_nodes(n), M(n * n);
+    for (int k = 0; k < n; ++k) {
+        double T0 = 1.0, T1 = t[k];
+        for (int i = 0; i < n; ++i) {
+            double Ti;
+            if (i == 0) Ti = T0;
+            else if (i == 1) Ti = T1;
+            else {
+                Ti = 2.0 * t[k] * T1 - T0;
+                T0 = T1;
+                T1 = Ti;
+            }
+            M[i * n + k] = (i == 0 ? 1.0 : 2.0) / n * Ti;
+        }
+    }
+    return M;
+}
+
+}  // namespace
+
+void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
+    auto t_start = std::chrono::steady_clock::now();
+    const int64_t n = p->n;
+    const int D = p->D, Ps = p->Ps, Pa = p->Pa, P = p->P;
+    cudaStream_t st;
+    IFGF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    Scratch S;
+
+    // 1. validation + bounding box
+    {
+        int nb = 148 * 4;
+        double* part = S.get<double>(6 * nb);
+        int* bad = S.get<int>(1);
+        IFGF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+        k_minmax<<<nb, TPB, 0, st>>>(pts, n, part, bad);
+        IFGF_CUDA(cudaGetLastError());
+        std::vector<double> h(6 * nb);
+        IFGF_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+        int hbad = d2h_one(bad, st);
+        if (hbad) throw Error{IFGF_EINVAL, "non-finite point coordinates"};
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int b = 0; b < nb; ++b)
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = std::min(lo[a], h[6 * b + a]);
+                hi[a] = std::max(hi[a], h[6 * b + 3 + a]);
+            }
+        // Root box (reading R9)
+        if (o.has_root) {
+            for (int a = 0; a < 3; ++a) p->root_c[a] = o.root_center[a];
+            p->H1 = o.root_side;
+        } else {
+            double ext = 0.0;
+            for (int a = 0; a < 3; ++a) {
+                p->root_c[a] = (lo[a] + hi[a]) / 2.0;
+                ext = std::max(ext, hi[a] - lo[a]);
+            }
+            if (ext == 0.0) {
+                if (n > 1) throw Error{IFGF_EDOMAIN, "zero-extent point cloud"};
+                ext = 1.0;
+            }
+            p->H1 = (1.0 + std::ldexp(1.0, -20)) * ext;
+        }
+        for (int a = 0; a < 3; ++a) p->x0[a] = p->root_c[a] - p->H1 / 2.0;
+    }
+
+    // 2. levels, cone grids (readings R5, R6, R8) and tables
+    p->lev.assign(D + 1, LevelHost());
+    for (int d = 1; d <= D; ++d) {
+        LevelParams& L = p->lev[d].p;
+        L.d = d;
+        L.H = std::ldexp(p->H1, -(d - 1));
+        for (int a = 0; a < 3; ++a) L.x0[a] = p->x0[a];
+    }
+    p->lev[D].p.ns = o.leaf_ns > 0 ? o.leaf_ns : 1;
+    p->lev[D].p.nC = o.leaf_nc > 0 ? o.leaf_nc : 2;
+    for (int d = D; d >= 2; --d) {
+        bool refine = p->k * p->lev[d - 1].p.H > 1.0;
+        p->lev[d - 1].p.ns = refine ? 2 * p->lev[d].p.ns : p->lev[d].p.ns;
+        p->lev[d - 1].p.nC = refine ? 2 * p->lev[d].p.nC : p->lev[d].p.nC;
+    }
+    const std::vector<double> ts = cheb_nodes(Ps), ta = cheb_nodes(Pa);
+    for (int d = 1; d <= D; ++d) {
+        LevelHost& LH = p->lev[d];
+        LevelParams& L = LH.p;
+        const double eta = std::sqrt(3.0) / 3.0;
+        L.h = std::sqrt(3.0) / 2.0 * L.H;
+        L.ds = eta / L.ns;
+        L.dth = kPi / L.nC;
+        L.ncell = 2LL * L.ns * (int64_t)L.nC * L.nC;
+        L.W = (L.ncell + 63) / 64;
+        if (d < 3) continue;  // no relevant segments at levels 1-2
+        if (L.ncell > (int64_t)1 << 31) throw Error{IFGF_ENOMEM, "cone grid too fine for the cell index"};
+        std::vector<double> ctb(L.nC + 1), cph(2 * L.nC + 1), sph(2 * L.nC + 1);
+        for (int kk = 0; kk <= L.nC; ++kk) ctb[kk] = std::cos((double)kk * kPi / (double)L.nC);
+        for (int j = 0; j < L.nC; ++j) {
+            double a = (double)j * kPi / (double)L.nC;
+            cph[j] = std::cos(a);
+            sph[j] = std::sin(a);
+            cph[j + L.nC] = -cph[j];
+            sph[j + L.nC] = -sph[j];
+        }
+        cph[2 * L.nC] = cph[0];
+        sph[2 * L.nC] = sph[0];
+        std::vector<double> rt(L.ns * Ps), stt(L.nC * Pa), ctt(L.nC * Pa), spt(2 * L.nC * Pa), cpt(2 * L.nC * Pa);
+        for (int is = 0; is < L.ns; ++is)
+            for (int ks = 0; ks < Ps; ++ks) {
+                double s = ((double)is + (1.0 + ts[ks]) / 2.0) * L.ds;
+                rt[is * Ps + ks] = L.h / s;
+            }
+        for (int it = 0; it < L.nC; ++it)
+            for (int kt = 0; kt < Pa; ++kt) {
+                double th = ((double)it + (1.0 + ta[kt]) / 2.0) * L.dth;
+                stt[it * Pa + kt] = std::sin(th);
+                ctt[it * Pa + kt] = std::cos(th);
+            }
+        for (int ip = 0; ip < 2 * L.nC; ++ip)
+            for (int kp = 0; kp < Pa; ++kp) {
+                double ph = ((double)ip + (1.0 + ta[kp]) / 2.0) * L.dth;
+                spt[ip * Pa + kp] = std::sin(ph);
+                cpt[ip * Pa + kp] = std::cos(ph);
+            }
+        L.cos_tb = LH.cos_tb = upload(p, ctb, st);
+        L.cphi = LH.cphi = upload(p, cph, st);
+        L.sphi = LH.sphi = upload(p, sph, st);
+        L.rtab = LH.rtab = upload(p, rt, st);
+        L.st_tab = LH.st_tab = upload(p, stt, st);
+        L.ct_tab = LH.ct_tab = upload(p, ctt, st);
+        L.sp_tab = LH.sp_tab = upload(p, spt, st);
+        L.cp_tab = LH.cp_tab = upload(p, cpt, st);
+    }
+    p->cheb_Ms = upload(p, cheb_fit_matrix(Ps), st);
+    p->cheb_Ma = upload(p, cheb_fit_matrix(Pa), st);
+
+    // 3. Morton keys + radix sort (relevant boxes via integer quotients)
+    uint64_t* keys_sorted = S.get<uint64_t>(n);
+    {
+        uint64_t* keys = S.get<uint64_t>(n);
+        int* idx = S.get<int>(n);
+        p->perm = dev_alloc<int>(p, n);
+        k_keys<<<nblocks(n), TPB, 0, st>>>(pts, n, p->x0[0], p->x0[1], p->x0[2], p->lev[D].p.H, 1 << (D - 1), keys,
+                                           idx);
+        IFGF_CUDA(cudaGetLastError());
+        size_t bytes = 0;
+        int bits = 3 * (D - 1);
+        if (bits < 1) bits = 1;
+        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys_sorted, idx, p->perm, (int)n, 0, bits, st));
+        void* tmp = S.get<char>((int64_t)bytes);
+        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys_sorted, idx, p->perm, (int)n, 0, bits, st));
+        IFGF_CUDA(cudaStreamSynchronize(st));
+        S.release(tmp);
+        S.release(keys);
+        S.release(idx);
+    }
+    p->px = dev_alloc<double>(p, n);
+    p->py = dev_alloc<double>(p, n);
+    p->pz = dev_alloc<double>(p, n);
+    k_gather_points<<<nblocks(n), TPB, 0, st>>>(pts, p->perm, n, p->px, p->py, p->pz);
+    IFGF_CUDA(cudaGetLastError());
+
+    // 4. boxes per level (leaf from points, coarser from finer)
+    std::vector<uint64_t*> bkey(D + 1, nullptr);
+    {
+        int* flag = S.get<int>(n);
+        int* incl = S.get<int>(n);
+        k_flag_runs<<<nblocks(n), TPB, 0, st>>>(keys_sorted, n, 0, flag);
+        inclusive_scan(S, flag, incl, n, st);
+        int64_t nbD = d2h_one(incl + n - 1, st);
+        LevelHost& LD = p->lev[D];
+        LD.p.nbox = nbD;
+        LD.box_start = dev_alloc<int>(p, nbD + 1);
+        bkey[D] = S.get<uint64_t>(nbD);
+        k_leaf_boxes<<<nblocks(n), TPB, 0, st>>>(keys_sorted, flag, incl, n, LD.box_start, bkey[D]);
+        int nn = (int)n;
+        IFGF_CUDA(cudaMemcpyAsync(LD.box_start + nbD, &nn, sizeof(int), cudaMemcpyHostToDevice, st));
+        IFGF_CUDA(cudaStreamSynchronize(st));
+        S.release(flag);
+        S.release(incl);
+        S.release(keys_sorted);
+        for (int d = D; d >= 2; --d) {
+            LevelHost& L = p->lev[d];
+            LevelHost& LP = p->lev[d - 1];
+            int64_t nb = L.p.nbox;
+            int* f = S.get<int>(nb);
+            int* inc = S.get<int>(nb);
+            k_flag_runs<<<nblocks(nb), TPB, 0, st>>>(bkey[d], nb, 3, f);
+            inclusive_scan(S, f, inc, nb, st);
+            int64_t nbp = d2h_one(inc + nb - 1, st);
+            LP.p.nbox = nbp;
+            L.box_parent = dev_alloc<int>(p, nb);
+            LP.box_start = dev_alloc<int>(p, nbp + 1);
+            LP.child_start = dev_alloc<int>(p, nbp + 1);
+            bkey[d - 1] = S.get<uint64_t>(nbp);
+            k_parent_boxes<<<nblocks(nb), TPB, 0, st>>>(bkey[d], L.box_start, f, inc, nb, L.box_parent, LP.box_start,
+                                                        bkey[d - 1], LP.child_start);
+            int nn2 = (int)n, nb2 = (int)nb;
+            IFGF_CUDA(cudaMemcpyAsync(LP.box_start + nbp, &nn2, sizeof(int), cudaMemcpyHostToDevice, st));
+            IFGF_CUDA(cudaMemcpyAsync(LP.child_start + nbp, &nb2, sizeof(int), cudaMemcpyHostToDevice, st));
+            IFGF_CUDA(cudaStreamSynchronize(st));
+            S.release(f);
+            S.release(inc);
+        }
+        for (int d = 1; d <= D; ++d) {
+            LevelHost& L = p->lev[d];
+            L.box_ijk = dev_alloc<int>(p, 3 * L.p.nbox);
+            k_box_ijk<<<nblocks(L.p.nbox), TPB, 0, st>>>(bkey[d], L.p.nbox, L.box_ijk);
+            IFGF_CUDA(cudaGetLastError());
+        }
+    }
+    // pairwise-different points
+    {
+        int* bad = S.get<int>(1);
+        IFGF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+        k_coincident<<<(int)p->lev[D].p.nbox, 64, 0, st>>>(p->px, p->py, p->pz, p->lev[D].box_start,
+                                                            p->lev[D].p.nbox, bad);
+        if (d2h_one(bad, st)) throw Error{IFGF_EDOMAIN, "coincident points (the paper requires pairwise-different points)"};
+    }
+
+    // 5. neighbours and cousins
+    for (int d = 1; d <= D; ++d) {
+        LevelHost& L = p->lev[d];
+        int64_t nb = L.p.nbox;
+        int* cnt = S.get<int>(nb);
+        k_neighbours<<<nblocks(nb), TPB, 0, st>>>(bkey[d], L.box_ijk, nb, 1 << (d - 1), 0, cnt, nullptr, nullptr);
+        L.nbr_off = csr_offsets(p, S, cnt, nb, st, &L.nnbr);
+        L.nbr_idx = dev_alloc<int>(p, L.nnbr);
+        k_neighbours<<<nblocks(nb), TPB, 0, st>>>(bkey[d], L.box_ijk, nb, 1 << (d - 1), 1, nullptr, L.nbr_off,
+                                                  L.nbr_idx);
+        IFGF_CUDA(cudaGetLastError());
+        if (d >= 3) {
+            LevelHost& LP = p->lev[d - 1];
+            k_cousins<<<nblocks(nb), TPB, 0, st>>>(L.box_ijk, L.box_parent, nb, LP.nbr_off, LP.nbr_idx, LP.child_start,
+                                                   0, cnt, nullptr, nullptr);
+            L.cou_off = csr_offsets(p, S, cnt, nb, st, &L.ncou);
+            L.cou_idx = dev_alloc<int>(p, L.ncou);
+            k_cousins<<<nblocks(nb), TPB, 0, st>>>(L.box_ijk, L.box_parent, nb, LP.nbr_off, LP.nbr_idx, LP.child_start,
+                                                   1, nullptr, L.cou_off, L.cou_idx);
+            IFGF_CUDA(cudaGetLastError());
+        }
+        // warp work items over all boxes of the level (targets)
+        if (d >= 3 || d == D) {
+            k_witem_count<<<nblocks(nb), TPB, 0, st>>>(L.box_start, nb, cnt);
+            int64_t ni = 0;
+            int* off = csr_offsets(p, S, cnt, nb, st, &ni);
+            L.witems = dev_alloc<int2>(p, ni);
+            L.p.nwitems = ni;
+            k_witem_fill<<<nblocks(nb), TPB, 0, st>>>(L.box_start, nb, off, L.witems);
+            IFGF_CUDA(cudaGetLastError());
+        }
+        S.release(cnt);
+    }
+    for (int d = 1; d <= D; ++d) S.release(bkey[d]);
+
+    // 6. source partition: owned leaf range -> owned box range per level
+    {
+        LevelHost& LD = p->lev[D];
+        int64_t nleaf = LD.p.nbox;
+        int64_t L0 = 0, L1 = nleaf;
+        if (p->nranks > 1) {
+            // work weight per leaf: points^2 (near + s2c proxy) + points * levels (cousin proxy)
+            std::vector<int> starts(nleaf + 1);
+            IFGF_CUDA(cudaMemcpy(starts.data(), LD.box_start, sizeof(int) * (nleaf + 1), cudaMemcpyDeviceToHost));
+            std::vector<double> w(nleaf);
+            for (int64_t b = 0; b < nleaf; ++b) {
+                double m = starts[b + 1] - starts[b];
+                w[b] = 14.0 * m * m + 8.0 * P * m + 45.0 * 4.0 * (D - 2) * m;
+            }
+            std::vector<int64_t> bounds(p->nranks + 1);
+            ifgf_status ps = ifgf_partition(w.data(), nleaf, p->nranks, bounds.data());
+            if (ps != IFGF_OK) throw Error{ps, "partition failed"};
+            L0 = bounds[p->rank];
+            L1 = bounds[p->rank + 1];
+        }
+        p->stats.owned_leaf_begin = L0;
+        p->stats.owned_leaf_end = L1;
+        int64_t a = L0, b = L1 - 1;  // inclusive leaf range (may be empty)
+        for (int d = D; d >= 1; --d) {
+            LevelHost& L = p->lev[d];
+            if (L1 <= L0) {
+                L.p.b0 = L.p.b1 = 0;
+                continue;
+            }
+            L.p.b0 = a;
+            L.p.b1 = b + 1;
+            if (d > 1) {
+                a = d2h_one(L.box_parent + a, st);
+                b = d2h_one(L.box_parent + b, st);
+            }
+        }
+    }
+
+    // publish pointers into LevelParams
+    for (int d = 1; d <= D; ++d) {
+        LevelHost& L = p->lev[d];
+        L.p.box_ijk = L.box_ijk;
+        L.p.box_start = L.box_start;
+        L.p.box_parent = L.box_parent;
+        L.p.child_start = L.child_start;
+        L.p.nbr_off = L.nbr_off;
+        L.p.nbr_idx = L.nbr_idx;
+        L.p.cou_off = L.cou_off;
+        L.p.cou_idx = L.cou_idx;
+        L.p.witems = L.witems;
+    }
+
+    // 7. relevant cone segments, single sweep d = 3..D
+    int* bad = S.get<int>(1);
+    IFGF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    for (int d = 3; d <= D; ++d) {
+        LevelHost& L = p->lev[d];
+        int64_t nown = L.p.b1 - L.p.b0;
+        int64_t nw = nown * L.p.W;
+        L.bitmap = dev_alloc<unsigned long long>(p, nw);
+        L.rank = dev_alloc<unsigned>(p, nw + 1);
+        L.p.bitmap = L.bitmap;
+        L.p.rank = L.rank;
+        IFGF_CUDA(cudaMemsetAsync(L.bitmap, 0, sizeof(unsigned long long) * (size_t)std::max<int64_t>(nw, 1), st));
+        if (nown > 0) {
+            k_flag_cousin_points<<<nblocks(L.p.nwitems * 32), TPB, 0, st>>>(L.p, p->px, p->py, p->pz, L.bitmap, bad);
+            IFGF_CUDA(cudaGetLastError());
+            if (d >= 4 && p->lev[d - 1].p.nseg > 0) {
+                LevelParams& LP = p->lev[d - 1].p;
+                k_flag_parent_nodes<<<nblocks(LP.nseg * P), TPB, 0, st>>>(L.p, LP, Ps, Pa, L.bitmap, bad);
+                IFGF_CUDA(cudaGetLastError());
+            }
+        }
+        // compaction: global exclusive prefix of popcounts -> rank; emit (box, cell) list
+        int64_t nseg = 0;
+        if (nw > 0) {
+            unsigned* pc = S.get<unsigned>(nw + 1);
+            k_popc<<<nblocks(nw), TPB, 0, st>>>(L.bitmap, nw, pc);
+            IFGF_CUDA(cudaMemsetAsync(pc + nw, 0, sizeof(unsigned), st));
+            exclusive_scan(S, pc, L.rank, nw + 1, st);
+            nseg = d2h_one(L.rank + nw, st);
+            S.release(pc);
+        }
+        if (nseg >= ((int64_t)1 << 31)) throw Error{IFGF_ENOMEM, "too many relevant segments in one level"};
+        L.p.nseg = nseg;
+        L.seg_box = dev_alloc<int>(p, nseg);
+        L.seg_cell = dev_alloc<int>(p, nseg);
+        L.p.seg_box = L.seg_box;
+        L.p.seg_cell = L.seg_cell;
+        if (nseg > 0) {
+            k_emit_segments<<<nblocks(nw), TPB, 0, st>>>(L.bitmap, L.rank, nw, L.p.W, L.p.b0, L.seg_box, L.seg_cell);
+            IFGF_CUDA(cudaGetLastError());
+        }
+        IFGF_CUDA(cudaStreamSynchronize(st));
+    }
+    if (d2h_one(bad, st)) throw Error{IFGF_EINTERNAL, "classification produced a cell outside the grid"};
+
+    // 8. stats (algorithmic work units)
+    {
+        ifgf_stats& s = p->stats;
+        s.n = n;
+        s.levels = D;
+        s.P_s = Ps;
+        s.P_ang = Pa;
+        s.P = P;
+        s.k = p->k;
+        for (int a = 0; a < 3; ++a) s.root_center[a] = p->root_c[a];
+        s.root_side = p->H1;
+        unsigned long long* acc = S.get<unsigned long long>(4 * (D + 2));
+        IFGF_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 4 * (D + 2), st));
+        k_stat_near<<<nblocks(p->lev[D].p.nbox), TPB, 0, st>>>(p->lev[D].p, acc);
+        if (D >= 3 && p->lev[D].p.nseg > 0)
+            k_stat_s2c<<<nblocks(p->lev[D].p.nseg), TPB, 0, st>>>(p->lev[D].p, P, acc + 1);
+        for (int d = 3; d <= D; ++d) {
+            k_stat_cousin<<<nblocks(p->lev[d].p.nbox), TPB, 0, st>>>(p->lev[d].p, acc + 4 * d);
+            if (d > 3 && p->lev[d - 1].p.nseg > 0)
+                k_stat_up<<<nblocks(p->lev[d - 1].p.nseg), TPB, 0, st>>>(p->lev[d].p, p->lev[d - 1].p, P,
+                                                                          acc + 4 * d + 1);
+        }
+        IFGF_CUDA(cudaGetLastError());
+        std::vector<unsigned long long> h(4 * (D + 2));
+        IFGF_CUDA(cudaMemcpyAsync(h.data(), acc, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
+        IFGF_CUDA(cudaStreamSynchronize(st));
+        s.near_pairs = (int64_t)h[0];
+        s.s2c_pairs = (int64_t)h[1];
+        for (int d = 1; d <= D; ++d) {
+            s.nbox[d] = p->lev[d].p.nbox;
+            s.nseg[d] = p->lev[d].p.nseg;
+            s.ns[d] = p->lev[d].p.ns;
+            s.nC[d] = p->lev[d].p.nC;
+            s.cousin_evals[d] = d >= 3 ? (int64_t)h[4 * d] : 0;
+            s.upward_evals[d] = d >= 4 ? (int64_t)h[4 * d + 1] : 0;
+            s.segment_bytes[d] = 16LL * P * p->lev[d].p.nseg;
+        }
+    }
+
+    // 9. apply scratch: permuted densities, sorted field, two segment-value levels
+    p->a_sorted = dev_alloc<double2>(p, n);
+    p->out_sorted = dev_alloc<double2>(p, n);
+    for (int par = 0; par < 2; ++par) {
+        int64_t mx = 0;
+        for (int d = 3; d <= D; ++d)
+            if ((d & 1) == par) mx = std::max(mx, p->lev[d].p.nseg);
+        p->vals_cap[par] = mx * P;
+        p->vals[par] = dev_alloc<double2>(p, mx * P);
+    }
+    IFGF_CUDA(cudaStreamSynchronize(st));
+    p->stats.plan_device_bytes = p->device_bytes;
+    p->stats.plan_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+}  // namespace ifgf

@@ -1,0 +1,269 @@
+"""Thin ctypes binding of libifgf.so (include/ifgf.h).
+
+Argument marshalling only: every step of the IFGF path runs in the library's
+CUDA kernels.  PyTorch supplies device memory, streams and (for multi-GPU)
+``torch.distributed``; there is no CPU fallback -- importing this module on a
+box without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libifgf.so")
+
+IFGF_STAGE_NEAR, IFGF_STAGE_COUSIN, IFGF_STAGE_UPWARD, IFGF_STAGE_ALL = 1, 2, 4, 7
+MAX_LEVELS = 22
+NUM_KCLASS = 7
+KCLASS_NAMES = ["permute", "near", "s2c", "fit", "cousin", "upward", "unpermute"]
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libifgf.so not built ({LIB_PATH}); run __graft_entry__.build()")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+
+class IfgfOpts(ctypes.Structure):
+    _fields_ = [
+        ("leaf_ns", ctypes.c_int), ("leaf_nc", ctypes.c_int),
+        ("has_root", ctypes.c_int), ("root_center", ctypes.c_double * 3), ("root_side", ctypes.c_double),
+        ("stage_mask", ctypes.c_uint), ("device", ctypes.c_int),
+        ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
+        ("reserved", ctypes.c_int * 8),
+    ]
+
+
+_L1 = MAX_LEVELS + 1
+
+
+class IfgfStats(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("levels", ctypes.c_int), ("P_s", ctypes.c_int), ("P_ang", ctypes.c_int), ("P", ctypes.c_int),
+        ("k", ctypes.c_double), ("root_center", ctypes.c_double * 3), ("root_side", ctypes.c_double),
+        ("owned_leaf_begin", ctypes.c_int64), ("owned_leaf_end", ctypes.c_int64),
+        ("nbox", ctypes.c_int64 * _L1), ("nseg", ctypes.c_int64 * _L1),
+        ("ns", ctypes.c_int * _L1), ("nC", ctypes.c_int * _L1),
+        ("near_pairs", ctypes.c_int64), ("s2c_pairs", ctypes.c_int64),
+        ("cousin_evals", ctypes.c_int64 * _L1), ("upward_evals", ctypes.c_int64 * _L1),
+        ("segment_bytes", ctypes.c_int64 * _L1),
+        ("plan_device_bytes", ctypes.c_int64), ("plan_ms", ctypes.c_double),
+    ]
+
+
+_c_p, _c_i, _c_i64, _c_d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+_SIGS = {
+    "ifgf_opts_init": ([ctypes.POINTER(IfgfOpts)], _c_i),
+    "ifgf_plan": ([_c_p, _c_i64, _c_d, _c_i, _c_i, _c_i, ctypes.POINTER(IfgfOpts), ctypes.POINTER(_c_p)], _c_i),
+    "ifgf_apply": ([_c_p, _c_p, _c_p, _c_p], _c_i),
+    "ifgf_apply_host": ([_c_p, _c_p, _c_p, _c_p], _c_i),
+    "ifgf_plan_destroy": ([_c_p], _c_i),
+    "ifgf_plan_stats": ([_c_p, ctypes.POINTER(IfgfStats)], _c_i),
+    "ifgf_plan_level_segments": ([_c_p, _c_i, _c_p, _c_i64, ctypes.POINTER(_c_i64)], _c_i),
+    "ifgf_profile_enable": ([_c_p, _c_i], _c_i),
+    "ifgf_profile_read": ([_c_p, _c_p, _c_p, _c_i], _c_i),
+    "ifgf_direct": ([_c_p, _c_i64, _c_d, _c_p, _c_p, _c_i64, _c_p, _c_p], _c_i),
+    "ifgf_partition": ([_c_p, _c_i64, _c_i, _c_p], _c_i),
+    "ifgf_bench_dfma": ([_c_i64, ctypes.POINTER(_c_d), ctypes.POINTER(_c_d), _c_p], _c_i),
+    "ifgf_status_string": ([_c_i], ctypes.c_char_p),
+    "ifgf_last_error_message": ([], ctypes.c_char_p),
+    "ifgf_version": ([], ctypes.c_char_p),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_SIGS)
+
+
+class IfgfError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        msg = _lib.ifgf_last_error_message().decode()
+        super().__init__(f"{where}: {_lib.ifgf_status_string(code).decode()}: {msg}")
+
+
+def _check(code: int, where: str):
+    if code != 0:
+        raise IfgfError(code, where)
+
+
+def _stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _f64_cuda(x: torch.Tensor, name: str) -> torch.Tensor:
+    if not (isinstance(x, torch.Tensor) and x.is_cuda):
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if x.dtype != torch.float64:
+        raise TypeError(f"{name} must be float64")
+    return x.contiguous()
+
+
+def _c128_cuda(x: torch.Tensor, name: str) -> torch.Tensor:
+    if not (isinstance(x, torch.Tensor) and x.is_cuda):
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if x.dtype != torch.complex128:
+        raise TypeError(f"{name} must be complex128")
+    return x.contiguous()
+
+
+class Plan:
+    """IFGF plan: ``ifgf_plan(points, k, levels, P_s, P_ang)`` (C ABI).
+
+    points: float64 [N, 3] CUDA tensor.  ``rank``/``nranks`` select this
+    process's source partition (``apply`` then returns the partial field and,
+    if ``group`` is given, all-reduces it with torch.distributed).
+    """
+
+    def __init__(self, points: torch.Tensor, k: float, levels: int, P_s: int = 3, P_ang: int = 5, *,
+                 leaf_ns: int = 0, leaf_nc: int = 0, root=None, stage_mask: int = 0, rank: int = 0,
+                 nranks: int = 1, group=None):
+        pts = _f64_cuda(points, "points")
+        if pts.dim() != 2 or pts.shape[1] != 3:
+            raise ValueError("points must be [N, 3]")
+        self.n = int(pts.shape[0])
+        self.device = pts.device
+        self.group = group
+        o = IfgfOpts()
+        _check(_lib.ifgf_opts_init(ctypes.byref(o)), "ifgf_opts_init")
+        o.leaf_ns, o.leaf_nc = int(leaf_ns), int(leaf_nc)
+        if root is not None:
+            o.has_root = 1
+            for a in range(3):
+                o.root_center[a] = float(root[0][a])
+            o.root_side = float(root[1])
+        o.stage_mask = int(stage_mask)
+        o.device = pts.device.index if pts.device.index is not None else torch.cuda.current_device()
+        o.rank, o.nranks = int(rank), int(nranks)
+        h = ctypes.c_void_p()
+        torch.cuda.synchronize(pts.device)
+        _check(_lib.ifgf_plan(pts.data_ptr(), self.n, float(k), int(levels), int(P_s), int(P_ang), ctypes.byref(o),
+                              ctypes.byref(h)), "ifgf_plan")
+        self._h = h
+        self.k, self.levels, self.P_s, self.P_ang = float(k), int(levels), int(P_s), int(P_ang)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.ifgf_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def apply(self, a: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """out = I(a) (complex128 [N] CUDA tensors, caller's point order)."""
+        a = _c128_cuda(a, "densities")
+        if a.shape != (self.n,):
+            raise ValueError("densities must be [N]")
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.complex128, device=a.device)
+        elif not out.is_contiguous() or out.dtype != torch.complex128 or out.shape != (self.n,):
+            raise ValueError("out must be a contiguous complex128 [N] tensor")
+        _check(_lib.ifgf_apply(self._h, a.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "ifgf_apply")
+        if self.group is not None:
+            allreduce_field(out, self.group)
+        return out
+
+    def apply_host(self, a_host: np.ndarray | torch.Tensor, out_host=None, stream=None):
+        """End-to-end apply from host buffers (ifgf_apply_host): H2D, apply, D2H, sync."""
+        if isinstance(a_host, torch.Tensor):
+            a = a_host.contiguous()
+            assert a.dtype == torch.complex128 and not a.is_cuda
+            ptr = a.data_ptr()
+        else:
+            a = np.ascontiguousarray(a_host, dtype=np.complex128)
+            ptr = a.ctypes.data
+        if out_host is None:
+            out_host = torch.empty(self.n, dtype=torch.complex128, pin_memory=True)
+        optr = out_host.data_ptr() if isinstance(out_host, torch.Tensor) else out_host.ctypes.data
+        _check(_lib.ifgf_apply_host(self._h, ptr, optr, _stream_ptr(stream)), "ifgf_apply_host")
+        return out_host
+
+    def stats(self) -> dict:
+        s = IfgfStats()
+        _check(_lib.ifgf_plan_stats(self._h, ctypes.byref(s)), "ifgf_plan_stats")
+        D = s.levels
+        lv = range(1, D + 1)
+        return dict(
+            n=s.n, levels=D, P_s=s.P_s, P_ang=s.P_ang, P=s.P, k=s.k,
+            root_center=list(s.root_center), root_side=s.root_side,
+            owned_leaf_range=(s.owned_leaf_begin, s.owned_leaf_end),
+            nbox={d: s.nbox[d] for d in lv}, nseg={d: s.nseg[d] for d in lv},
+            grid={d: (s.ns[d], s.nC[d]) for d in lv},
+            near_pairs=s.near_pairs, s2c_pairs=s.s2c_pairs,
+            cousin_evals={d: s.cousin_evals[d] for d in lv}, upward_evals={d: s.upward_evals[d] for d in lv},
+            segment_bytes={d: s.segment_bytes[d] for d in lv},
+            plan_device_bytes=s.plan_device_bytes, plan_ms=s.plan_ms,
+        )
+
+    def level_segments(self, d: int) -> np.ndarray:
+        cnt = ctypes.c_int64()
+        _check(_lib.ifgf_plan_level_segments(self._h, d, None, 0, ctypes.byref(cnt)), "ifgf_plan_level_segments")
+        out = np.zeros((cnt.value, 4), dtype=np.int64)
+        if cnt.value:
+            _check(_lib.ifgf_plan_level_segments(self._h, d, out.ctypes.data, cnt.value, ctypes.byref(cnt)),
+                   "ifgf_plan_level_segments")
+        return out
+
+    def profile_enable(self, on: bool = True):
+        _check(_lib.ifgf_profile_enable(self._h, 1 if on else 0), "ifgf_profile_enable")
+
+    def profile_read(self, reset: bool = True) -> dict:
+        ms = np.zeros(NUM_KCLASS)
+        ln = np.zeros(NUM_KCLASS, dtype=np.int64)
+        _check(_lib.ifgf_profile_read(self._h, ms.ctypes.data, ln.ctypes.data, 1 if reset else 0),
+               "ifgf_profile_read")
+        return {KCLASS_NAMES[c]: (float(ms[c]), int(ln[c])) for c in range(NUM_KCLASS)}
+
+
+def allreduce_field(field: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum the ranks' partial fields in place (the one exchange step of the
+    source-partitioned matvec; NCCL over NVLink on GPUs, gloo in CPU tests)."""
+    import torch.distributed as dist
+    dist.all_reduce(torch.view_as_real(field), op=dist.ReduceOp.SUM, group=group)
+    return field
+
+
+def direct(points: torch.Tensor, k: float, a: torch.Tensor, targets: torch.Tensor, stream=None) -> torch.Tensor:
+    """GPU direct sum at target indices (measurement harness; eq. field1)."""
+    pts = _f64_cuda(points, "points")
+    a = _c128_cuda(a, "densities")
+    t = targets.to(device=pts.device, dtype=torch.int64).contiguous()
+    out = torch.empty(t.shape[0], dtype=torch.complex128, device=pts.device)
+    _check(_lib.ifgf_direct(pts.data_ptr(), pts.shape[0], float(k), a.data_ptr(), t.data_ptr(), t.shape[0],
+                            out.data_ptr(), _stream_ptr(stream)), "ifgf_direct")
+    return out
+
+
+def partition(weights, nranks: int) -> np.ndarray:
+    """Host-only work-weighted contiguous partition (ifgf_partition)."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    b = np.zeros(nranks + 1, dtype=np.int64)
+    _check(_lib.ifgf_partition(w.ctypes.data, w.shape[0], int(nranks), b.ctypes.data), "ifgf_partition")
+    return b
+
+
+def bench_dfma(iters: int = 20000, stream=None):
+    """Measured FP64 FMA throughput (FLOP/s) and kernel ms on the current device."""
+    f, ms = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.ifgf_bench_dfma(int(iters), ctypes.byref(f), ctypes.byref(ms), _stream_ptr(stream)),
+           "ifgf_bench_dfma")
+    return f.value, ms.value
+
+
+def version() -> str:
+    return _lib.ifgf_version().decode()

@@ -1,0 +1,220 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bar (BASELINE.json north_star): relative l2 <= 1e-11 vs the oracle; error vs the
+direct sum <= 1.1 x the oracle's own; discrete plan decisions bit-identical.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2010_02857_b200 import inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+PARITY = 1e-11
+
+
+@pytest.fixture(scope="module")
+def ifgf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2010_02857_b200 import ifgf as m
+    return m
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda:0")
+
+
+def run_gpu(ifgf, pts, a, k, D, Ps=3, Pa=5, **kw):
+    plan = ifgf.Plan(dev(pts), k, D, Ps, Pa, **kw)
+    out = plan.apply(dev(a)).cpu().numpy()
+    st = plan.stats()  # also raises if an apply met an invariant violation
+    return plan, out, st
+
+
+def segs_sorted(x):
+    x = np.asarray(x, dtype=np.int64).reshape(-1, 4)
+    return x[np.lexsort((x[:, 3], x[:, 2], x[:, 1], x[:, 0]))]
+
+
+# ------------------------------------------------------------------ cfg1
+@pytest.fixture(scope="module")
+def cfg1_runs(ifgf):
+    c = inputs.CONFIGS["cfg1"]
+    pts, a = c.points(), c.densities()
+    oplan = oracle.OraclePlan(pts, c.k, c.levels, c.Ps, c.Pang)
+    ref = oplan.apply(a)
+    plan, got, st = run_gpu(ifgf, pts, a, c.k, c.levels, c.Ps, c.Pang)
+    return c, pts, a, oplan, ref, plan, got, st
+
+
+def test_cfg1_parity_all_points(cfg1_runs):
+    c, pts, a, oplan, ref, plan, got, st = cfg1_runs
+    assert oracle.rel_l2(got, ref) <= PARITY
+
+
+def test_cfg1_error_vs_full_direct_sum(cfg1_runs, ifgf):
+    """cfg1 is compared to the full O(N^2) direct sum (BASELINE.json configs[0])."""
+    c, pts, a, oplan, ref, plan, got, st = cfg1_runs
+    tg = np.arange(c.n)
+    exact = ifgf.direct(dev(pts), c.k, dev(a), dev(tg)).cpu().numpy()
+    sample = inputs.error_targets(c.n, 500)
+    np.testing.assert_allclose(exact[sample], oracle.direct(pts, c.k, a, sample), rtol=1e-12, atol=1e-13)
+    e_gpu, e_or = oracle.rel_l2(got, exact), oracle.rel_l2(ref, exact)
+    assert e_gpu <= 1.1 * e_or
+
+
+def test_cfg1_plan_diff(cfg1_runs):
+    """Per level: relevant boxes and the sorted (box, cell) keys are identical."""
+    c, pts, a, oplan, ref, plan, got, st = cfg1_runs
+    for d in range(1, c.levels + 1):
+        assert st["nbox"][d] == oplan.level_info(d)["nbox"]
+        assert st["grid"][d] == (oplan.level_info(d)["ns"], oplan.level_info(d)["nC"])
+        np.testing.assert_array_equal(segs_sorted(plan.level_segments(d)), segs_sorted(oplan.level_segments(d)))
+
+
+def test_cfg1_stage_masks(cfg1_runs, ifgf):
+    c, pts, a, oplan, ref, plan, got, st = cfg1_runs
+    for mask in (ifgf.IFGF_STAGE_NEAR, ifgf.IFGF_STAGE_NEAR | ifgf.IFGF_STAGE_COUSIN, ifgf.IFGF_STAGE_COUSIN):
+        _, g, _ = run_gpu(ifgf, pts, a, c.k, c.levels, stage_mask=mask)
+        r = oplan.apply(a, stage_mask=mask)
+        assert oracle.rel_l2(g, r) <= PARITY, mask
+
+
+def test_apply_host_and_reuse(cfg1_runs):
+    """ifgf_apply_host (host buffers, e2e path) equals ifgf_apply; the plan is reusable."""
+    c, pts, a, oplan, ref, plan, got, st = cfg1_runs
+    h = plan.apply_host(a).numpy()
+    assert np.array_equal(h, got)
+    b = inputs.densities(c.n, seed=3)
+    assert oracle.rel_l2(plan.apply(dev(b)).cpu().numpy(), oplan.apply(b)) <= PARITY
+
+
+def test_linearity_and_determinism(cfg1_runs):
+    c, pts, a, oplan, ref, plan, got, st = cfg1_runs
+    b = inputs.densities(c.n, seed=11)
+    al, be = 0.7 + 0.2j, -1.1 + 0.4j
+    lhs = plan.apply(dev(al * a + be * b)).cpu().numpy()
+    rhs = al * got + be * plan.apply(dev(b)).cpu().numpy()
+    assert oracle.rel_l2(lhs, rhs) < 1e-12
+    again = plan.apply(dev(a)).cpu().numpy()
+    assert np.array_equal(again, got)
+
+
+# ---------------------------------------------------- ragged / small / edge
+@pytest.mark.parametrize("n,D", [(1, 3), (2, 2), (2, 4), (7, 3), (100, 1), (100, 2), (333, 3), (1000, 4),
+                                 (4099, 5), (5000, 6)])
+def test_small_and_ragged(ifgf, n, D):
+    rng = np.random.default_rng(n + D)
+    pts = inputs.fibonacci_sphere(n) * rng.uniform(0.5, 2.0)
+    a = inputs.densities(n, seed=n)
+    k = 9.0
+    _, got, _ = run_gpu(ifgf, pts, a, k, D)
+    ref = oracle.OraclePlan(pts, k, D, 3, 5).apply(a)
+    if n == 1:
+        assert np.all(got == 0)
+    else:
+        assert oracle.rel_l2(got, ref) <= PARITY
+
+
+@pytest.mark.parametrize("Ps,Pa", [(5, 5), (4, 6), (1, 1), (2, 3), (7, 9)])
+def test_orders_generic_and_specialised(ifgf, Ps, Pa):
+    """(3,5) and (5,5) run specialised kernels; the rest the runtime-order path."""
+    n = 6000
+    pts = inputs.fibonacci_sphere(n, (1.0, 1.0, 0.25))
+    a = inputs.densities(n)
+    k = 20.0
+    _, got, _ = run_gpu(ifgf, pts, a, k, 5, Ps, Pa)
+    ref = oracle.OraclePlan(pts, k, 5, Ps, Pa).apply(a)
+    assert oracle.rel_l2(got, ref) <= PARITY
+
+
+def test_leaf_grid_and_laplace(ifgf):
+    n = 5000
+    pts = inputs.rough_sphere(n)
+    a = inputs.densities(n)
+    for k, ns, nc in [(0.0, 1, 2), (15.0, 2, 3), (15.0, 1, 4)]:
+        _, got, _ = run_gpu(ifgf, pts, a, k, 5, leaf_ns=ns, leaf_nc=nc)
+        ref = oracle.OraclePlan(pts, k, 5, 3, 5, leaf_ns=ns, leaf_nc=nc).apply(a)
+        assert oracle.rel_l2(got, ref) <= PARITY, (k, ns, nc)
+
+
+def test_centred_source_exact(ifgf):
+    """One unit source exactly at a leaf centre, D = 3: the result is exact (no
+    interpolation error): GPU equals the direct sum to rounding."""
+    rng = np.random.default_rng(4)
+    pts = rng.uniform(-1.99, 1.99, (600, 3))
+    pts[0] = [0.5, 0.5, -0.5]
+    a = np.zeros(len(pts), dtype=complex)
+    a[0] = 1.0
+    _, got, _ = run_gpu(ifgf, pts, a, 3.0, 3, root=([0.0, 0.0, 0.0], 4.0))
+    ref = oracle.direct(pts, 3.0, a, np.arange(len(pts)))
+    assert oracle.rel_l2(got, ref) < 1e-14
+
+
+def test_metamorphic_rotation(ifgf):
+    n = 8000
+    pts = inputs.fibonacci_sphere(n)
+    a = inputs.densities(n)
+    _, I, _ = run_gpu(ifgf, pts, a, 25.0, 5)
+    rot = np.stack([-pts[:, 1], pts[:, 0], pts[:, 2]], axis=1)
+    _, J, _ = run_gpu(ifgf, rot, a, 25.0, 5)
+    assert oracle.rel_l2(J, I) < 1e-12
+
+
+def test_errors(ifgf):
+    pts = inputs.fibonacci_sphere(100)
+    with pytest.raises(ifgf.IfgfError) as e:
+        ifgf.Plan(dev(np.concatenate([pts, pts[:1]])), 1.0, 3, 3, 5)
+    assert e.value.code == 2
+    with pytest.raises(ifgf.IfgfError) as e:
+        ifgf.Plan(dev(np.zeros((4, 3))), 1.0, 3, 3, 5)
+    assert e.value.code == 2
+    bad = pts.copy()
+    bad[5, 1] = np.nan
+    with pytest.raises(ifgf.IfgfError) as e:
+        ifgf.Plan(dev(bad), 1.0, 3, 3, 5)
+    assert e.value.code == 1
+    for kw in [dict(k=-1.0), dict(levels=0), dict(levels=23), dict(P_s=0), dict(P_ang=17)]:
+        args = dict(k=1.0, levels=3, P_s=3, P_ang=5)
+        args.update(kw)
+        with pytest.raises(ifgf.IfgfError) as e:
+            ifgf.Plan(dev(pts), args["k"], args["levels"], args["P_s"], args["P_ang"])
+        assert e.value.code == 1
+
+
+def test_multirank_emulation_one_gpu(ifgf):
+    """Source partition by work-weighted Morton leaf ranges: the per-rank partial
+    fields (run sequentially on one GPU) sum to the single-GPU field."""
+    c = inputs.CONFIGS["cfg1"]
+    pts, a = c.points(), c.densities()
+    _, full, _ = run_gpu(ifgf, pts, a, c.k, c.levels)
+    for R in (2, 3, 8):
+        acc = np.zeros_like(full)
+        covered = []
+        for r in range(R):
+            p, part, st = run_gpu(ifgf, pts, a, c.k, c.levels, rank=r, nranks=R)
+            covered.append(st["owned_leaf_range"])
+            acc += part
+        assert covered[0][0] == 0 and all(covered[i][1] == covered[i + 1][0] for i in range(R - 1))
+        assert oracle.rel_l2(acc, full) < 1e-13, R
+
+
+# ------------------------------------------------------------ larger configs
+@pytest.mark.slow
+def test_cfg2_parity(ifgf):
+    c = inputs.CONFIGS["cfg2"]
+    pts, a = c.points(), c.densities()
+    oplan = oracle.OraclePlan(pts, c.k, c.levels, c.Ps, c.Pang)
+    ref = oplan.apply(a)
+    plan, got, st = run_gpu(ifgf, pts, a, c.k, c.levels, c.Ps, c.Pang)
+    assert oracle.rel_l2(got, ref) <= PARITY
+    for d in range(3, c.levels + 1):
+        assert st["nseg"][d] == oplan.level_info(d)["nseg"]
+    tg = inputs.error_targets(c.n, 1000)
+    exact = ifgf.direct(dev(pts), c.k, dev(a), dev(tg)).cpu().numpy()
+    assert oracle.rel_l2(got[tg], exact) <= 1.1 * oracle.rel_l2(ref[tg], exact)
