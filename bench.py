@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""IFGF matvec benchmark (BASELINE.json metric: "IFGF matvec points/s (fp64
+complex) at 1/2/4/8 B200; rel. error vs direct sum").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = one full IFGF operator application (the whole hot path: permute,
+near field, source-to-cone, per-level fit / cousin / upward, un-permute; plus
+the NCCL all-reduce of the partial fields when N > 1) on synthetic inputs
+resident in HBM.  Prints ONE JSON line on rank 0.
+
+--impl reference times the oracle (oracle/, serial C++) on a bounded sample of
+the same workload family on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2010_02857_b200 import inputs  # noqa: E402
+
+METRIC = "IFGF matvec points/s (fp64 complex) at 1/2/4/8 B200; rel. error vs direct sum"
+UNIT = "points/s"
+
+# Bounded CPU sample for the oracle (cpu_baseline and --impl reference): the same
+# workload family as cfg4 (Fibonacci sphere, 22 points per wavelength, leaves of
+# lambda/4, (P_s, P_ang) = (3, 5)) scaled down to 4 lambda: N = 24,576, k = 4 pi, D = 5.
+CPU_SAMPLE = dict(n=24_576, k=4 * math.pi, levels=5, Ps=3, Pang=5)
+CPU_SAMPLE_DESC = ("oracle apply (serial C++, 1 thread) on the cfg4 workload family scaled to 4 lambda: "
+                   "Fibonacci sphere N=24,576, k=4pi, D=5 (leaves lambda/4 as cfg4), (P_s,P_ang)=(3,5)")
+
+
+def algorithmic_flops_per_upward_eval(Ps: int, Pa: int) -> float:
+    """separable tensor contraction (complex x real MAC = 4
+    flops) 4 (P + P_s P_ang + P_s) + recentering complex MAC (8)."""
+    return 4.0 * (Ps * Pa * Pa + Ps * Pa + Ps) + 8.0
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm, smax, power, reasons = [], None, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+def time_oracle_sample(repeats: int = 1):
+    import oracle
+    c = CPU_SAMPLE
+    pts = inputs.fibonacci_sphere(c["n"])
+    a = inputs.densities(c["n"])
+    plan = oracle.OraclePlan(pts, c["k"], c["levels"], c["Ps"], c["Pang"])
+    ts = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        plan.apply(a)
+        ts.append(time.perf_counter() - t0)
+    return c["n"], ts
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    n, ts = time_oracle_sample(args.warmup + args.steps)
+    timed = ts[args.warmup:] if len(ts) > args.warmup else ts
+    t = sum(timed) / len(timed)
+    value = n / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CPU_SAMPLE_DESC},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": CPU_SAMPLE_DESC},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_02857_b200 import ifgf
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    group = dist.group.WORLD if world > 1 else None
+    c = inputs.CONFIGS[args.config]
+
+    pts_h = c.points()
+    a_h = c.densities()
+    pts = torch.from_numpy(pts_h).to(dev)
+    a = torch.from_numpy(a_h).to(dev)
+    del pts_h
+
+    dfma_flops, _ = ifgf.bench_dfma(20000)  # measured FP64 FMA peak (roofline denominator)
+
+    t0 = time.perf_counter()
+    plan = ifgf.Plan(pts, c.k, c.levels, c.Ps, c.Pang, rank=rank, nranks=world, group=group)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+    st = plan.stats()
+    out = torch.empty(c.n, dtype=torch.complex128, device=dev)
+
+    for _ in range(args.warmup):
+        plan.apply(a, out)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K applies, inputs resident in HBM
+    plan.profile_enable(True)
+    plan.profile_read(reset=True)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.apply(a, out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    prof = plan.profile_read(reset=True)
+    plan.profile_enable(False)
+    t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms_max = float(t_ms.item())
+    ms_per_step = ms_max / args.steps
+    value = c.n / (ms_per_step * 1e-3)
+
+    # ---------------- end to end: host buffers in, host result out, every step
+    a_pin = torch.from_numpy(a_h).pin_memory()
+    out_pin = torch.empty(c.n, dtype=torch.complex128).pin_memory()
+    if world == 1:
+        plan.apply_host(a_pin, out_pin)  # warm
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        if world == 1:
+            plan.apply_host(a_pin, out_pin)  # C ABI: H2D, apply, D2H, sync
+        else:
+            a_dev = a_pin.to(dev, non_blocking=True)
+            plan.apply(a_dev, out)  # includes the NCCL all-reduce
+            out_pin.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e2.elapsed_time(e3)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = c.n / (float(te.item()) / args.steps * 1e-3)
+
+    # ---------------- accuracy vs the direct sum (after timing; not in the metric)
+    plan.apply(a, out)
+    tg = torch.from_numpy(inputs.error_targets(c.n, 1000)).to(dev)
+    exact = ifgf.direct(pts, c.k, a, tg)
+    got = out[tg]
+    rel_err = float(torch.sqrt(torch.sum(torch.abs(got - exact) ** 2) / torch.sum(torch.abs(exact) ** 2)).item())
+
+    # ---------------- roofline of the dominant kernel (K7 upward, FP64 pipe)
+    up_ms, up_launch = prof["upward"]
+    up_evals = sum(st["upward_evals"].values())  # per apply (this rank)
+    flops_apply = up_evals * algorithmic_flops_per_upward_eval(c.Ps, c.Pang)
+    achieved = flops_apply * args.steps / (up_ms * 1e-3) if up_ms > 0 else 0.0
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"{args.config}:upward_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    launches = sum(v[1] for v in prof.values())
+    kernel_ms = {k: v[0] / args.steps for k, v in prof.items()}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            n_s, ts = time_oracle_sample(args.cpu_repeats)
+            cpu = {"value": n_s / statistics.median(ts), "unit": UNIT, "cores": 1, "kind": "oracle",
+                   "sample": CPU_SAMPLE_DESC + f"; median of {len(ts)} applies ({sum(ts):.1f} s of CPU work)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"{c.name}: {c.geometry} {c.scale}, k={c.k / math.pi:.0f}pi ({c.k / math.pi:.0f} lambda across), "
+                            f"N={c.n}, D={c.levels}, (P_s,P_ang)=({c.Ps},{c.Pang}), Fibonacci points, "
+                            "splitmix64 densities",
+                "N": c.n, "k": c.k, "levels": c.levels, "P_s": c.Ps, "P_ang": c.Pang,
+                "parallelism": f"source-partition x{world} (Morton leaf ranges) + NCCL all-reduce" if world > 1
+                else "1 GPU",
+                "l2": "inputs larger than L2: each apply streams "
+                      f"{sum(st['segment_bytes'].values()) / 1e9:.1f} GB of cone-segment data",
+            },
+            "rel_err_vs_direct": rel_err,
+            "plan_ms": plan_s * 1e3,
+            "kernel_ms_per_step": kernel_ms,
+            "roofline": {"kernel": "K7 upward (k_upward)", "bound": "alu", "achieved": achieved / 1e12,
+                         "peak": dfma_flops / 1e12, "unit": "TFLOP/s", "frac": achieved / dfma_flops,
+                         "traffic": traffic,
+                         "peak_source": "FP64 DFMA microbenchmark (ifgf_bench_dfma) measured in this run; "
+                                        "nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s",
+                         "flops_per_unit": algorithmic_flops_per_upward_eval(c.Ps, c.Pang),
+                         "units_per_step": up_evals},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * c.n, "d2h_bytes_per_step": 16 * c.n},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4", choices=sorted(inputs.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-repeats", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -283,6 +283,83 @@ __global__ void __launch_bounds__(TPB) k_upward(LevelParams L, LevelParams LP, c
     vals_p[sp * P + n] = make_double2(ar, ai);
 }
 
+// K7, cell-grouped: the child-relative geometry of a parent node (child cell,
+// local coordinates, recentering factor) depends only on (cell gamma', node,
+// child octant), not on the box.  One block per chunk of <= kChunk parent
+// segments that share gamma' (thread = node): the geometry of each octant is
+// computed once and reused for every segment of the chunk; all threads of the
+// block evaluate the same child box at the same time (L1-broadcast loads).
+template <int PS, int PA>
+__global__ void __launch_bounds__(128, 4) k_upward_g(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
+                                                  double k, double2* vals_p, int* bad) {
+    constexpr int P = PS * PA * PA;
+    constexpr int CH = kChunk;
+    constexpr int NT = ((P + 31) / 32) * 32;
+    __shared__ int sh_seg[CH];
+    __shared__ int sh_child[CH][8];
+    __shared__ unsigned sh_omask;
+    __shared__ double2 sh_acc[CH][NT];
+    const int64_t c = blockIdx.x;
+    const int s0 = LP.chunk_start[c];
+    const int s1 = (c + 1 < LP.nchunk) ? LP.chunk_start[c + 1] : (int)LP.nseg;
+    const int cnt = min(CH, s1 - s0);
+    if (threadIdx.x == 0) sh_omask = 0u;
+    __syncthreads();
+    for (int t = threadIdx.x; t < CH * 8; t += blockDim.x) {
+        int j = t >> 3, o = t & 7;
+        int B = -1;
+        if (j < cnt) {
+            int seg = LP.cell_seg[s0 + j];
+            if (o == 0) sh_seg[j] = seg;
+            B = LP.child_oct[8 * LP.seg_box[seg] + o];
+            if (B < L.b0 || B >= L.b1) B = -1;
+            if (B >= 0) atomicOr(&sh_omask, 1u << o);
+        }
+        sh_child[j][o] = B;
+    }
+    __syncthreads();
+    const int n = threadIdx.x;
+    if (n >= P) return;
+    const unsigned omask = sh_omask;
+    double off[3];
+    node_off(LP, PS, PA, LP.seg_cell[sh_seg[0]], n, off);
+    const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
+    const double hh = 0.5 * L.H;
+    for (int j = 0; j < cnt; ++j) sh_acc[j][n] = make_double2(0.0, 0.0);
+    for (int o = 0; o < 8; ++o) {
+        if (!((omask >> o) & 1u)) continue;
+        const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
+        Cls cl = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+        const int64_t cell = cell_of(L, cl);
+        double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
+        double diff = num / (cl.r + rQ);
+        double ratio = rQ / cl.r;
+        double sn, cs;
+        sincos(k * diff, &sn, &cs);
+        const double rr = ratio * cs, ri = ratio * sn;
+        double Ts[PS], Tt[PA];
+        cheb_T<PS>(cl.us, Ts);
+        cheb_T<PA>(cl.ut, Tt);
+        const double up = cl.up;
+#pragma unroll 1
+        for (int j = 0; j < cnt; ++j) {
+            const int B = sh_child[j][o];
+            if (B < 0) continue;
+            const int64_t slot = seg_slot(L, B, cell);
+            if (slot < 0) {
+                atomicOr(bad, 1);
+                continue;
+            }
+            double2 F = contract<PS, PA>(vals_d + slot * P, Ts, Tt, up);
+            double2 acc = sh_acc[j][n];
+            acc.x = fma(rr, F.x, fma(-ri, F.y, acc.x));
+            acc.y = fma(rr, F.y, fma(ri, F.x, acc.y));
+            sh_acc[j][n] = acc;
+        }
+    }
+    for (int j = 0; j < cnt; ++j) vals_p[(int64_t)sh_seg[j] * P + n] = sh_acc[j][n];
+}
+
 // ------------------------------------------------------------- dispatch
 template <int PS, int PA>
 struct Kern {
@@ -292,6 +369,14 @@ struct Kern {
     }
     static void upward(dim3 g, cudaStream_t st, const LevelParams& L, const LevelParams& LP, const ifgf_plan_s* p,
                        const double2* vd, double2* vp, int* bad) {
+        if constexpr (PS > 0 && PS * PA * PA <= 128) {
+            if (LP.nchunk > 0 && !p->legacy_upward) {
+                constexpr int P = PS * PA * PA;
+                const int threads = ((P + 31) / 32) * 32;
+                k_upward_g<PS, PA><<<(unsigned)LP.nchunk, threads, 0, st>>>(L, LP, vd, p->k, vp, bad);
+                return;
+            }
+        }
         k_upward<PS, PA><<<g, TPB, 0, st>>>(L, LP, vd, p->k, p->Ps, p->Pa, vp, bad);
     }
 };

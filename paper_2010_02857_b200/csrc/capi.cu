@@ -3,6 +3,7 @@
 // measurement kernel, the FP64 roofline microbenchmark and the partitioner.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -184,6 +185,7 @@ ifgf_status ifgf_plan(const double* points, int64_t n, double k, int levels, int
     p->Ps = P_s;
     p->Pa = P_ang;
     p->P = P_s * P_ang * P_ang;
+    if (const char* e = std::getenv("IFGF_LEGACY_UPWARD")) p->legacy_upward = std::atoi(e);
     p->stage_mask = o.stage_mask ? o.stage_mask : IFGF_STAGE_ALL;
     p->rank = o.nranks > 1 ? o.rank : 0;
     p->nranks = o.nranks > 1 ? o.nranks : 1;

@@ -76,7 +76,17 @@ struct LevelParams {  // passed by value to kernels
     // K6 warp work items (box, first point)
     const int2* witems;
     int64_t nwitems;
+    // children of each box by octant ((i&1)<<2 | (j&1)<<1 | (k&1)) at level d + 1, -1 if absent
+    const int* child_oct;
+    // segments grouped by cone cell (box-independent K7 geometry): cell_seg = segment
+    // indices sorted by (cell, segment); chunk_start = first position of each chunk
+    // of <= kChunk segments sharing one cell
+    const int* cell_seg;
+    const int* chunk_start;
+    int64_t nchunk;
 };
+
+constexpr int kChunk = 16;
 
 struct LevelHost {
     LevelParams p{};
@@ -89,6 +99,7 @@ struct LevelHost {
     double *cos_tb = nullptr, *cphi = nullptr, *sphi = nullptr;
     double *rtab = nullptr, *st_tab = nullptr, *ct_tab = nullptr, *sp_tab = nullptr, *cp_tab = nullptr;
     int2* witems = nullptr;
+    int *child_oct = nullptr, *cell_seg = nullptr, *chunk_start = nullptr;
     int64_t ncou = 0, nnbr = 0;
     std::vector<int> box_ijk_host;  // kept for plan export (small levels only)
 };
@@ -130,6 +141,7 @@ struct ifgf_plan_s {
     };
     std::vector<PendingEv> pending;
     int* dev_bad = nullptr;  // device flag: apply-time invariant violation (EINTERNAL)
+    int legacy_upward = 0;   // env IFGF_LEGACY_UPWARD=1: per-evaluation-geometry K7 (A/B testing)
     int64_t device_bytes = 0;
     std::vector<void*> allocs;  // every cudaMalloc of the plan
 };
@@ -247,12 +259,11 @@ __device__ __forceinline__ void cheb_T_rt(int n, double u, double* T) {
 // Evaluate the tensor Chebyshev interpolant with coefficients C (layout
 // ((c * PA + b) * PS + a) for s-index a, theta-index b, phi-index c) at local
 // coordinates (us, ut, up): contraction over phi, then theta, then s.
+// The phi loop is kept rolled (T_c by recurrence) so that only one phi-slab of
+// P_ang * P_s coefficients is in flight per thread (register pressure).
 template <int PS, int PA>
-__device__ __forceinline__ double2 eval_interp(const double2* __restrict__ C, double us, double ut, double up) {
-    double Ts[PS], Tt[PA], Tp[PA];
-    cheb_T<PS>(us, Ts);
-    cheb_T<PA>(ut, Tt);
-    cheb_T<PA>(up, Tp);
+__device__ __forceinline__ double2 contract(const double2* __restrict__ C, const double* Ts, const double* Tt,
+                                            double up) {
     double wr[PA * PS], wi[PA * PS];
 #pragma unroll
     for (int i = 0; i < PA * PS; ++i) {
@@ -260,14 +271,20 @@ __device__ __forceinline__ double2 eval_interp(const double2* __restrict__ C, do
         wr[i] = v.x;
         wi[i] = v.y;
     }
-#pragma unroll
+    double tm1 = 1.0, t = up;
+    const double u2 = 2.0 * up;
+#pragma unroll 1
     for (int c = 1; c < PA; ++c) {
+        const double2* __restrict__ Cc = C + c * PA * PS;
 #pragma unroll
         for (int i = 0; i < PA * PS; ++i) {
-            double2 v = __ldg(C + c * PA * PS + i);
-            wr[i] = fma(Tp[c], v.x, wr[i]);
-            wi[i] = fma(Tp[c], v.y, wi[i]);
+            double2 v = __ldg(Cc + i);
+            wr[i] = fma(t, v.x, wr[i]);
+            wi[i] = fma(t, v.y, wi[i]);
         }
+        const double tn = fma(u2, t, -tm1);
+        tm1 = t;
+        t = tn;
     }
     double xr[PS], xi[PS];
 #pragma unroll
@@ -289,6 +306,14 @@ __device__ __forceinline__ double2 eval_interp(const double2* __restrict__ C, do
         fi = fma(Ts[a], xi[a], fi);
     }
     return make_double2(fr, fi);
+}
+
+template <int PS, int PA>
+__device__ __forceinline__ double2 eval_interp(const double2* __restrict__ C, double us, double ut, double up) {
+    double Ts[PS], Tt[PA];
+    cheb_T<PS>(us, Ts);
+    cheb_T<PA>(ut, Tt);
+    return contract<PS, PA>(C, Ts, Tt, up);
 }
 
 // Runtime-order fallback (any P_s, P_ang <= kMaxP1).

@@ -309,6 +309,37 @@ __global__ void k_emit_segments(const unsigned long long* __restrict__ bm, const
     }
 }
 
+// ------------------------------------------- K7 grouping by cone cell
+__global__ void k_child_oct(const int* __restrict__ child_start, const int* __restrict__ ijk_child, int64_t nb,
+                            int* child_oct) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    for (int o = 0; o < 8; ++o) child_oct[8 * b + o] = -1;
+    for (int ch = child_start[b]; ch < child_start[b + 1]; ++ch) {
+        int o = ((ijk_child[3 * ch] & 1) << 2) | ((ijk_child[3 * ch + 1] & 1) << 1) | (ijk_child[3 * ch + 2] & 1);
+        child_oct[8 * b + o] = ch;
+    }
+}
+__global__ void k_iota(int64_t n, int* v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (int)i;
+}
+__global__ void k_run_start(const int* __restrict__ key, int64_t n, int* rs) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) rs[i] = (i == 0 || key[i] != key[i - 1]) ? (int)i : 0;
+}
+__global__ void k_chunk_flag(const int* __restrict__ rs, int64_t n, int ch, int* flag) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = ((i - rs[i]) % ch == 0) ? 1 : 0;
+}
+__global__ void k_chunk_emit(const int* __restrict__ flag, const int* __restrict__ incl, int64_t n, int* start) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) start[incl[i] - 1] = (int)i;
+}
+struct MaxOp {
+    __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
+};
+
 // ---------------------------------------------------------------- stats
 __global__ void k_stat_near(LevelParams L, unsigned long long* acc) {
     int64_t T = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -777,6 +808,55 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         IFGF_CUDA(cudaStreamSynchronize(st));
     }
     if (d2h_one(bad, st)) throw Error{IFGF_EINTERNAL, "classification produced a cell outside the grid"};
+
+    // 7b. K7 support: children by octant; parent segments grouped by cone cell
+    for (int d = 1; d < D; ++d) {
+        LevelHost& L = p->lev[d];
+        L.child_oct = dev_alloc<int>(p, 8 * L.p.nbox);
+        k_child_oct<<<nblocks(L.p.nbox), TPB, 0, st>>>(L.child_start, p->lev[d + 1].box_ijk, L.p.nbox, L.child_oct);
+        IFGF_CUDA(cudaGetLastError());
+        L.p.child_oct = L.child_oct;
+        const int64_t ns = L.p.nseg;
+        if (d < 3 || ns == 0) continue;
+        int* vals_in = S.get<int>(ns);
+        int* keys_out = S.get<int>(ns);
+        L.cell_seg = dev_alloc<int>(p, ns);
+        k_iota<<<nblocks(ns), TPB, 0, st>>>(ns, vals_in);
+        int bits = 1;
+        while (bits < 31 && ((int64_t)1 << bits) < L.p.ncell) ++bits;
+        size_t bytes = 0;
+        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, L.seg_cell, keys_out, vals_in, L.cell_seg, (int)ns,
+                                                  0, bits, st));
+        void* tmp = S.get<char>((int64_t)bytes);
+        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, L.seg_cell, keys_out, vals_in, L.cell_seg, (int)ns, 0,
+                                                  bits, st));
+        S.release(tmp);
+        int* rs = S.get<int>(ns);
+        int* rsm = S.get<int>(ns);
+        k_run_start<<<nblocks(ns), TPB, 0, st>>>(keys_out, ns, rs);
+        bytes = 0;
+        IFGF_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, rs, rsm, MaxOp(), (int)ns, st));
+        tmp = S.get<char>((int64_t)bytes);
+        IFGF_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, rs, rsm, MaxOp(), (int)ns, st));
+        S.release(tmp);
+        int* flag = rs;  // reuse
+        k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, kChunk, flag);
+        int* incl = S.get<int>(ns);
+        inclusive_scan(S, flag, incl, ns, st);
+        int64_t nch = d2h_one(incl + ns - 1, st);
+        L.chunk_start = dev_alloc<int>(p, nch);
+        k_chunk_emit<<<nblocks(ns), TPB, 0, st>>>(flag, incl, ns, L.chunk_start);
+        IFGF_CUDA(cudaGetLastError());
+        IFGF_CUDA(cudaStreamSynchronize(st));
+        L.p.cell_seg = L.cell_seg;
+        L.p.chunk_start = L.chunk_start;
+        L.p.nchunk = nch;
+        S.release(vals_in);
+        S.release(keys_out);
+        S.release(rs);
+        S.release(rsm);
+        S.release(incl);
+    }
 
     // 8. stats (algorithmic work units)
     {
