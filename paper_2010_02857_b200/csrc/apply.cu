@@ -360,6 +360,284 @@ __global__ void __launch_bounds__(128, 4) k_upward_g(LevelParams L, LevelParams 
     for (int j = 0; j < cnt; ++j) vals_p[(int64_t)sh_seg[j] * P + n] = sh_acc[j][n];
 }
 
+// ---------------------------------------------------------------------------
+// K7, cell-grouped + shared-memory staged.  Per (chunk, octant) the nodes of
+// the block map to a handful (U) of child cells; those U child segments are
+// copied into shared memory with cp.async (double-buffered over the chunk's
+// segments) and every thread contracts from shared memory.  This turns the
+// per-evaluation chain of dependent global loads into one bulk, fully
+// overlapped copy per (segment, octant).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Tensor contraction from shared memory (same order as contract()).
+template <int PS, int PA>
+__device__ __forceinline__ double2 contract_sm(const double2* C, const double* Ts, const double* Tt, double up) {
+    double wr[PA * PS], wi[PA * PS];
+#pragma unroll
+    for (int i = 0; i < PA * PS; ++i) {
+        double2 v = C[i];
+        wr[i] = v.x;
+        wi[i] = v.y;
+    }
+    double tm1 = 1.0, t = up;
+    const double u2 = 2.0 * up;
+#pragma unroll
+    for (int c = 1; c < PA; ++c) {
+#pragma unroll
+        for (int i = 0; i < PA * PS; ++i) {
+            double2 v = C[c * PA * PS + i];
+            wr[i] = fma(t, v.x, wr[i]);
+            wi[i] = fma(t, v.y, wi[i]);
+        }
+        const double tn = fma(u2, t, -tm1);
+        tm1 = t;
+        t = tn;
+    }
+    double xr[PS], xi[PS];
+#pragma unroll
+    for (int a = 0; a < PS; ++a) {
+        xr[a] = wr[a];
+        xi[a] = wi[a];
+    }
+#pragma unroll
+    for (int b = 1; b < PA; ++b)
+#pragma unroll
+        for (int a = 0; a < PS; ++a) {
+            xr[a] = fma(Tt[b], wr[b * PS + a], xr[a]);
+            xi[a] = fma(Tt[b], wi[b * PS + a], xi[a]);
+        }
+    double fr = xr[0], fi = xi[0];
+#pragma unroll
+    for (int a = 1; a < PS; ++a) {
+        fr = fma(Ts[a], xr[a], fr);
+        fi = fma(Ts[a], xi[a], fi);
+    }
+    return make_double2(fr, fi);
+}
+
+template <int PS, int PA>
+struct StagedCfg {
+    static constexpr int P = PS * PA * PA;
+    static constexpr int NT = ((P + 31) / 32) * 32;
+    static constexpr int MAXU = P <= 80 ? 12 : 8;
+    static constexpr size_t smem = (size_t)(2 * MAXU * P + kChunk * NT) * sizeof(double2);
+};
+
+template <int PS, int PA>
+__global__ void __launch_bounds__(128, 3) k_upward_s(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
+                                                     double k, const double* __restrict__ Ms,
+                                                     const double* __restrict__ Ma, double2* vals_p, int* bad) {
+    using Cfg = StagedCfg<PS, PA>;
+    constexpr int P = Cfg::P, NT = Cfg::NT, MAXU = Cfg::MAXU, CH = kChunk;
+    extern __shared__ double2 dsm[];
+    double2* sh_coef = dsm;                 // [2][MAXU][P]
+    double2* sh_acc = dsm + 2 * MAXU * P;   // [CH][NT]
+    __shared__ int sh_seg[CH];
+    __shared__ int sh_child[CH][8];
+    __shared__ unsigned sh_omask;
+    __shared__ int sh_cell[NT];
+    __shared__ unsigned char sh_lead[NT];
+    __shared__ int sh_ucell[MAXU];
+    __shared__ int sh_slot[CH][MAXU];
+    __shared__ int sh_jl[CH];
+    __shared__ int sh_nj;
+    const int tid = threadIdx.x;
+    const int64_t c = blockIdx.x;
+    const int s0 = LP.chunk_start[c];
+    const int s1 = (c + 1 < LP.nchunk) ? LP.chunk_start[c + 1] : (int)LP.nseg;
+    const int cnt = min(CH, s1 - s0);
+    if (tid == 0) sh_omask = 0u;
+    __syncthreads();
+    for (int t = tid; t < CH * 8; t += NT) {
+        int j = t >> 3, o = t & 7;
+        int B = -1;
+        if (j < cnt) {
+            int seg = LP.cell_seg[s0 + j];
+            if (o == 0) sh_seg[j] = seg;
+            B = LP.child_oct[8 * LP.seg_box[seg] + o];
+            if (B < L.b0 || B >= L.b1) B = -1;
+            if (B >= 0) atomicOr(&sh_omask, 1u << o);
+        }
+        sh_child[j][o] = B;
+    }
+    __syncthreads();
+    const int n = tid;
+    const bool active = n < P;
+    const unsigned omask = sh_omask;
+    double off[3] = {0.0, 0.0, 0.0};
+    if (active) node_off(LP, PS, PA, LP.seg_cell[sh_seg[0]], n, off);
+    const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
+    const double hh = 0.5 * L.H;
+    for (int j = 0; j < cnt; ++j) sh_acc[j * NT + n] = make_double2(0.0, 0.0);
+    for (int o = 0; o < 8; ++o) {
+        if (!((omask >> o) & 1u)) continue;
+        const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
+        double rr = 0.0, ri = 0.0, up = 0.0;
+        double Ts[PS], Tt[PA];
+        int cellc = -1;
+        if (active) {
+            Cls cl = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+            cellc = (int)cell_of(L, cl);
+            double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
+            double diff = num / (cl.r + rQ);
+            double ratio = rQ / cl.r;
+            double sn, cs;
+            sincos(k * diff, &sn, &cs);
+            rr = ratio * cs;
+            ri = ratio * sn;
+            cheb_T<PS>(cl.us, Ts);
+            cheb_T<PA>(cl.ut, Tt);
+            up = cl.up;
+        }
+        sh_cell[n] = cellc;
+        __syncthreads();
+        // distinct child cells of this octant: leader = first node with the cell
+        int first = n;
+        if (active)
+            for (int m = 0; m < n; ++m)
+                if (sh_cell[m] == cellc) {
+                    first = m;
+                    break;
+                }
+        const bool lead = active && first == n;
+        sh_lead[n] = lead ? 1 : 0;
+        __syncthreads();
+        int myu = 0;
+        if (active)
+            for (int m = 0; m < first; ++m) myu += sh_lead[m];
+        if (lead && myu < MAXU) sh_ucell[myu] = cellc;
+        const int U = __syncthreads_count(lead);
+        if (U > MAXU) {
+            // rare: too many distinct cells to stage; evaluate from global memory
+            if (active)
+                for (int j = 0; j < cnt; ++j) {
+                    const int B = sh_child[j][o];
+                    if (B < 0) continue;
+                    const int64_t slot = seg_slot(L, B, cellc);
+                    if (slot < 0) {
+                        atomicOr(bad, 1);
+                        continue;
+                    }
+                    double2 F = contract<PS, PA>(vals_d + slot * P, Ts, Tt, up);
+                    double2 acc = sh_acc[j * NT + n];
+                    acc.x = fma(rr, F.x, fma(-ri, F.y, acc.x));
+                    acc.y = fma(rr, F.y, fma(ri, F.x, acc.y));
+                    sh_acc[j * NT + n] = acc;
+                }
+            __syncthreads();
+            continue;
+        }
+        for (int t = tid; t < cnt * U; t += NT) {
+            const int j = t / U, u = t - (t / U) * U;
+            const int B = sh_child[j][o];
+            int sl = -1;
+            if (B >= 0) {
+                int64_t s = seg_slot(L, B, sh_ucell[u]);
+                if (s < 0) atomicOr(bad, 1);
+                sl = (int)s;
+            }
+            sh_slot[j][u] = sl;
+        }
+        if (tid == 0) {
+            int nj = 0;
+            for (int j = 0; j < cnt; ++j)
+                if (sh_child[j][o] >= 0) sh_jl[nj++] = j;
+            sh_nj = nj;
+        }
+        __syncthreads();
+        const int nj = sh_nj;
+        auto issue = [&](int q, int buf) {
+            const int j = sh_jl[q];
+            double2* dst = sh_coef + buf * MAXU * P;
+            for (int t = tid; t < U * P; t += NT) {
+                const int u = t / P, i = t - (t / P) * P;
+                const int sl = sh_slot[j][u];
+                if (sl >= 0) cp_async16(dst + t, vals_d + (int64_t)sl * P + i);
+                else dst[t] = make_double2(0.0, 0.0);
+            }
+            cp_async_commit();
+        };
+        if (nj > 0) issue(0, 0);
+        for (int q = 0; q < nj; ++q) {
+            if (q + 1 < nj) {
+                issue(q + 1, (q + 1) & 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            if (active) {
+                const int j = sh_jl[q];
+                double2 F = contract_sm<PS, PA>(sh_coef + (q & 1) * MAXU * P + myu * P, Ts, Tt, up);
+                double2 acc = sh_acc[j * NT + n];
+                acc.x = fma(rr, F.x, fma(-ri, F.y, acc.x));
+                acc.y = fma(rr, F.y, fma(ri, F.x, acc.y));
+                sh_acc[j * NT + n] = acc;
+            }
+            __syncthreads();
+        }
+    }
+    // Fused K5: node values -> tensor Chebyshev coefficients (reading R1), three
+    // separable passes through shared memory; thread n produces coefficient n.
+    double ms[PS], mt[PA], mp[PA];
+    const int ia = n % PS, ib = (n / PS) % PA, ic = n / (PS * PA);
+    if (active) {
+#pragma unroll
+        for (int q = 0; q < PS; ++q) ms[q] = __ldg(Ms + ia * PS + q);
+#pragma unroll
+        for (int q = 0; q < PA; ++q) {
+            mt[q] = __ldg(Ma + ib * PA + q);
+            mp[q] = __ldg(Ma + ic * PA + q);
+        }
+    }
+    double2* tA = sh_coef;
+    double2* tB = sh_coef + P;
+    __syncthreads();
+    for (int j = 0; j < cnt; ++j) {
+        const double2* V = sh_acc + j * NT;
+        if (active) {  // along s
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int q = 0; q < PS; ++q) {
+                double2 v = V[(ic * PA + ib) * PS + q];
+                xr = fma(ms[q], v.x, xr);
+                xi = fma(ms[q], v.y, xi);
+            }
+            tA[n] = make_double2(xr, xi);
+        }
+        __syncthreads();
+        if (active) {  // along theta
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int q = 0; q < PA; ++q) {
+                double2 v = tA[(ic * PA + q) * PS + ia];
+                xr = fma(mt[q], v.x, xr);
+                xi = fma(mt[q], v.y, xi);
+            }
+            tB[n] = make_double2(xr, xi);
+        }
+        __syncthreads();
+        if (active) {  // along phi
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int q = 0; q < PA; ++q) {
+                double2 v = tB[(q * PA + ib) * PS + ia];
+                xr = fma(mp[q], v.x, xr);
+                xi = fma(mp[q], v.y, xi);
+            }
+            vals_p[(int64_t)sh_seg[j] * P + n] = make_double2(xr, xi);
+        }
+    }
+}
+
 // ------------------------------------------------------------- dispatch
 template <int PS, int PA>
 struct Kern {
@@ -367,17 +645,31 @@ struct Kern {
                        double2* out, int* bad) {
         k_cousin<PS, PA><<<g, TPB, 0, st>>>(L, p->px, p->py, p->pz, v, p->k, p->Ps, p->Pa, out, bad);
     }
-    static void upward(dim3 g, cudaStream_t st, const LevelParams& L, const LevelParams& LP, const ifgf_plan_s* p,
+    // returns true if the kernel also produced the Chebyshev coefficients (fused K5)
+    static bool upward(dim3 g, cudaStream_t st, const LevelParams& L, const LevelParams& LP, const ifgf_plan_s* p,
                        const double2* vd, double2* vp, int* bad) {
         if constexpr (PS > 0 && PS * PA * PA <= 128) {
-            if (LP.nchunk > 0 && !p->legacy_upward) {
+            if (LP.nchunk > 0 && p->legacy_upward == 0) {
+                using Cfg = StagedCfg<PS, PA>;
+                static bool attr = false;
+                if (!attr) {
+                    IFGF_CUDA(cudaFuncSetAttribute(k_upward_s<PS, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)Cfg::smem));
+                    attr = true;
+                }
+                k_upward_s<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(L, LP, vd, p->k, p->cheb_Ms,
+                                                                                      p->cheb_Ma, vp, bad);
+                return true;
+            }
+            if (LP.nchunk > 0 && p->legacy_upward == 2) {
                 constexpr int P = PS * PA * PA;
                 const int threads = ((P + 31) / 32) * 32;
                 k_upward_g<PS, PA><<<(unsigned)LP.nchunk, threads, 0, st>>>(L, LP, vd, p->k, vp, bad);
-                return;
+                return false;
             }
         }
         k_upward<PS, PA><<<g, TPB, 0, st>>>(L, LP, vd, p->k, p->Ps, p->Pa, vp, bad);
+        return false;
     }
 };
 
@@ -477,12 +769,13 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
                 Prof pr(p, st, 5);
                 dim3 g(nblk(LP.nseg * P));
                 double2* vp = p->vals[(d - 1) & 1];
+                bool fused = false;
                 dispatch(
-                    Ps, Pa, [&] { Kern<3, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
-                    [&] { Kern<5, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
-                    [&] { Kern<0, 0>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); });
+                    Ps, Pa, [&] { fused = Kern<3, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
+                    [&] { fused = Kern<5, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
+                    [&] { fused = Kern<0, 0>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); });
                 pr.done();
-                fit(d - 1);
+                if (!fused) fit(d - 1);
             }
         } else {
             have = false;

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "ifgf_internal.cuh"
@@ -324,7 +325,12 @@ __global__ void k_iota(int64_t n, int* v) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) v[i] = (int)i;
 }
-__global__ void k_run_start(const int* __restrict__ key, int64_t n, int* rs) {
+__global__ void k_tile_keys(const int* __restrict__ seg_box, const int* __restrict__ seg_cell, int64_t n,
+                            int64_t tile, int bits, uint64_t* key) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) key[i] = ((uint64_t)(seg_box[i] / tile) << bits) | (uint64_t)seg_cell[i];
+}
+__global__ void k_run_start(const uint64_t* __restrict__ key, int64_t n, int* rs) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) rs[i] = (i == 0 || key[i] != key[i - 1]) ? (int)i : 0;
 }
@@ -819,18 +825,30 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         const int64_t ns = L.p.nseg;
         if (d < 3 || ns == 0) continue;
         int* vals_in = S.get<int>(ns);
-        int* keys_out = S.get<int>(ns);
+        uint64_t* keys_in = S.get<uint64_t>(ns);
+        uint64_t* keys_out = S.get<uint64_t>(ns);
         L.cell_seg = dev_alloc<int>(p, ns);
         k_iota<<<nblocks(ns), TPB, 0, st>>>(ns, vals_in);
         int bits = 1;
         while (bits < 31 && ((int64_t)1 << bits) < L.p.ncell) ++bits;
+        // L2 tiles: consecutive parent boxes whose children's coefficients total
+        // ~32 MB; segments are grouped by cell only inside a tile (locality).
+        const double child_bytes_per_box =
+            (double)p->lev[d + 1].p.nseg * P * 16.0 / (double)std::max<int64_t>(1, L.p.b1 - L.p.b0);
+        double tile_bytes = 4096.0e6;  // child bytes per tile (env IFGF_TILE_MB)
+        if (const char* e = std::getenv("IFGF_TILE_MB")) tile_bytes = std::atof(e) * 1.0e6;
+        int64_t tile = (int64_t)std::max(1.0, tile_bytes / std::max(1.0, child_bytes_per_box));
+        int tbits = 1;
+        while (tbits < 32 && ((int64_t)1 << tbits) <= L.p.nbox / tile + 1) ++tbits;
+        k_tile_keys<<<nblocks(ns), TPB, 0, st>>>(L.seg_box, L.seg_cell, ns, tile, bits, keys_in);
         size_t bytes = 0;
-        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, L.seg_cell, keys_out, vals_in, L.cell_seg, (int)ns,
-                                                  0, bits, st));
+        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, keys_out, vals_in, L.cell_seg, (int)ns, 0,
+                                                  bits + tbits, st));
         void* tmp = S.get<char>((int64_t)bytes);
-        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, L.seg_cell, keys_out, vals_in, L.cell_seg, (int)ns, 0,
-                                                  bits, st));
+        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_in, keys_out, vals_in, L.cell_seg, (int)ns, 0,
+                                                  bits + tbits, st));
         S.release(tmp);
+        S.release(keys_in);
         int* rs = S.get<int>(ns);
         int* rsm = S.get<int>(ns);
         k_run_start<<<nblocks(ns), TPB, 0, st>>>(keys_out, ns, rs);
