@@ -176,6 +176,9 @@ ifgf_status ifgf_partition(const double* weights, int64_t nleaf, int nranks, int
  */
 ifgf_status ifgf_bench_dfma(int64_t iters, double* flops_per_s, double* ms, void* cuda_stream);
 
+/* Same for the FP64 tensor core (mma.sync m8n8k4 f64, DMMA): achieved FLOP/s. */
+ifgf_status ifgf_bench_dmma(int64_t iters, double* flops_per_s, double* ms, void* cuda_stream);
+
 const char* ifgf_status_string(ifgf_status s);
 const char* ifgf_last_error_message(void);
 const char* ifgf_version(void);

@@ -115,7 +115,55 @@ __global__ void k_dfma(int64_t iters, double seed, double* sink) {
     double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
     if (s == 1.2345) sink[0] = s;  // never true; keeps the chains alive
 }
+// FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) throughput probe: 8 independent
+// accumulator tiles per warp.
+__global__ void k_dmma(int64_t iters, double seed, double* sink) {
+    double a = seed + threadIdx.x * 1e-3, b = 0.5 + threadIdx.x * 1e-4;
+    double c[8][2];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = t;
+    for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(c[t][0]), "+d"(c[t][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+    if (s == 1.2345) sink[0] = s;
+}
 }  // namespace
+
+extern "C" ifgf_status ifgf_bench_dmma(int64_t iters, double* flops, double* ms, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    return guarded(nullptr, [&] {
+        int dev = 0, nsm = 0;
+        IFGF_CUDA(cudaGetDevice(&dev));
+        IFGF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        double* sink = nullptr;
+        IFGF_CUDA(cudaMallocAsync((void**)&sink, sizeof(double), st));
+        int blocks = nsm * 8, tpb = 256;
+        k_dmma<<<blocks, tpb, 0, st>>>(iters / 10 + 1, 1.0, sink);
+        cudaEvent_t e0, e1;
+        IFGF_CUDA(cudaEventCreate(&e0));
+        IFGF_CUDA(cudaEventCreate(&e1));
+        IFGF_CUDA(cudaEventRecord(e0, st));
+        k_dmma<<<blocks, tpb, 0, st>>>(iters, 1.0, sink);
+        IFGF_CUDA(cudaEventRecord(e1, st));
+        IFGF_CUDA(cudaEventSynchronize(e1));
+        float t = 0.f;
+        IFGF_CUDA(cudaEventElapsedTime(&t, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        IFGF_CUDA(cudaFreeAsync(sink, st));
+        // per warp per mma: 8 x 8 x 4 FMA = 512 flops
+        double f = 512.0 * 8.0 * (double)iters * blocks * (tpb / 32);
+        if (flops) *flops = f / (t * 1e-3);
+        if (ms) *ms = t;
+    });
+}
 
 namespace ifgf {
 void set_error(const std::string& msg) { g_last_error = msg; }

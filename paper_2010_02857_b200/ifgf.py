@@ -69,6 +69,7 @@ _SIGS = {
     "ifgf_direct": ([_c_p, _c_i64, _c_d, _c_p, _c_p, _c_i64, _c_p, _c_p], _c_i),
     "ifgf_partition": ([_c_p, _c_i64, _c_i, _c_p], _c_i),
     "ifgf_bench_dfma": ([_c_i64, ctypes.POINTER(_c_d), ctypes.POINTER(_c_d), _c_p], _c_i),
+    "ifgf_bench_dmma": ([_c_i64, ctypes.POINTER(_c_d), ctypes.POINTER(_c_d), _c_p], _c_i),
     "ifgf_status_string": ([_c_i], ctypes.c_char_p),
     "ifgf_last_error_message": ([], ctypes.c_char_p),
     "ifgf_version": ([], ctypes.c_char_p),
@@ -262,6 +263,14 @@ def bench_dfma(iters: int = 20000, stream=None):
     f, ms = ctypes.c_double(), ctypes.c_double()
     _check(_lib.ifgf_bench_dfma(int(iters), ctypes.byref(f), ctypes.byref(ms), _stream_ptr(stream)),
            "ifgf_bench_dfma")
+    return f.value, ms.value
+
+
+def bench_dmma(iters: int = 20000, stream=None):
+    """Measured FP64 tensor-core (DMMA m8n8k4) throughput (FLOP/s) and kernel ms."""
+    f, ms = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.ifgf_bench_dmma(int(iters), ctypes.byref(f), ctypes.byref(ms), _stream_ptr(stream)),
+           "ifgf_bench_dmma")
     return f.value, ms.value
 
 

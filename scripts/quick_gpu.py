@@ -20,4 +20,4 @@ tg = inputs.error_targets(c.n, 1000)
 ex = ifgf.direct(dp, c.k, da, torch.from_numpy(tg).cuda()).cpu().numpy()
 g = out.cpu().numpy()[tg]
 print('rel err vs direct', np.sqrt(np.sum(np.abs(g-ex)**2)/np.sum(np.abs(ex)**2)), flush=True)
-print('dfma', ifgf.bench_dfma(20000))
+print("dfma", ifgf.bench_dfma(20000)); print("dmma", ifgf.bench_dmma(20000))

@@ -218,3 +218,18 @@ def test_cfg2_parity(ifgf):
     tg = inputs.error_targets(c.n, 1000)
     exact = ifgf.direct(dev(pts), c.k, dev(a), dev(tg)).cpu().numpy()
     assert oracle.rel_l2(got[tg], exact) <= 1.1 * oracle.rel_l2(ref[tg], exact)
+
+
+@pytest.mark.parametrize("mode", ["1", "2", "3", "4"])
+def test_upward_kernel_variants(ifgf, mode, monkeypatch):
+    """Every K7 variant (1 per-evaluation geometry, 2 cell-grouped, 3 cell-grouped
+    + shared-memory staged, 4 FP64 tensor-core DMMA) matches the oracle; the
+    default (0) picks DMMA for dense chunks and the staged kernel otherwise."""
+    monkeypatch.setenv("IFGF_LEGACY_UPWARD", mode)
+    n = 20000
+    pts = inputs.fibonacci_sphere(n, (1.0, 1.0, 0.5))
+    a = inputs.densities(n, seed=21)
+    k = 6 * math.pi
+    _, got, _ = run_gpu(ifgf, pts, a, k, 5)
+    ref = oracle.OraclePlan(pts, k, 5, 3, 5).apply(a)
+    assert oracle.rel_l2(got, ref) <= PARITY
