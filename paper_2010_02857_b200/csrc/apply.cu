@@ -5,6 +5,7 @@
 //   K7 upward interpolation + recentering.
 // Every output has exactly one writer (target-major K3/K6, parent-node-major
 // K7): no atomics on values, deterministic results.
+#include <climits>
 #include <cmath>
 
 #include "ifgf_internal.cuh"
@@ -882,6 +883,385 @@ __global__ void __launch_bounds__(128, 2) k_upward_mma(LevelParams L, LevelParam
     }
 }
 
+// ---------------------------------------------------------------------------
+// K7 on the FP64 tensor core, large cell chunks (fine levels).
+//
+// Within a chunk of <= J parent segments sharing cone cell gamma' and a child
+// octant o, the child-relative geometry of parent node n (child cell u_n, local
+// coordinates, recentering factor rec_n = G(y,c_B)/G(y,c_Q)) is box-independent,
+// so for every child cell u
+//     V[j][n] += rec_n * sum_i W[n][i] C[B_{j,o}, u][i]       (u_n == u)
+// with the tensor Chebyshev basis W[n][i] = T_a(u_s) T_b(u_theta) T_c(u_phi)
+// (i = (c P_ang + b) P_s + a).  That is a dense (nodes x coefficients) x
+// (coefficients x segments) product: DMMA m8n8k4 tiles with rows = nodes
+// sorted by child cell, columns = the segments whose box has child o
+// (compacted per octant), k = coefficient index; real and imaginary parts share
+// the W fragment.  Per block:
+//   phase 0  segments, children by octant, per-octant compaction (warp ballots)
+//   phase 1  geometry of all (octant, node) pairs (classification contract)
+//   phase 2  per octant (one warp each): distinct child cells, node sort by cell
+//   phase 3  (octant, cell, segment) -> child segment slot (bitmap rank)
+//   phase 4  per octant: W_o into shared memory, then tasks (segment tile, cell):
+//            the warp loads the 8 child coefficient vectors once (B fragments in
+//            registers) and sweeps the node tiles of that cell (A fragments from
+//            shared memory); rows of other cells in a boundary tile are computed
+//            and discarded.  Each V entry has one writer per octant and octants
+//            are summed in a fixed order (deterministic, no atomics).
+//   phase 5  fused K5 fit of the chunk's node values -> Chebyshev coefficients.
+template <int PS, int PA>
+struct TcCfg {
+    static constexpr int P = PS * PA * PA;
+    static constexpr int KS = (P + 3) / 4;   // k-steps of 4
+    static constexpr int NR = (P + 7) / 8;   // row (node) tiles of 8
+    static constexpr int NW = NR * 8;
+    // W row stride (doubles): == 4 or 12 mod 16 makes the 8x4 A-fragment loads of
+    // each half-warp hit 16 distinct 8-byte bank pairs
+    static constexpr int KP = ((4 * KS) % 16 == 4 || (4 * KS) % 16 == 12) ? 4 * KS : 4 * KS + 4;
+    static constexpr int J = kChunkTC;
+    static constexpr int UM = 8;              // distinct child cells per octant with staged slots
+    static constexpr int NT = 384;
+    static constexpr int NWARP = NT / 32;
+    static constexpr int R = (NW + 31) / 32;
+    static constexpr int FG = 16;             // fit group (segments)
+    static constexpr size_t a16(size_t x) { return (x + 15) / 16 * 16; }
+    static constexpr size_t oV = 0;                                       // double2 [J][P]
+    static constexpr size_t oW = a16(oV + (size_t)J * P * 16);            // double [NW][KP]
+    static constexpr size_t oG = a16(oW + (size_t)NW * KP * 8);           // double [8][NW][5]
+    static constexpr size_t oU = a16(oG + (size_t)8 * NW * 5 * 8);        // int [8][NW]
+    static constexpr size_t oSlot = a16(oU + (size_t)8 * NW * 4);         // int [8][UM][J]
+    static constexpr size_t oChild = a16(oSlot + (size_t)8 * UM * J * 4); // int [8][J]
+    static constexpr size_t oSeg = a16(oChild + (size_t)8 * J * 4);       // int [J]
+    static constexpr size_t oUcell = a16(oSeg + (size_t)J * 4);           // int [8][UM]
+    static constexpr size_t oMisc = a16(oUcell + (size_t)8 * UM * 4);     // int U[8], nO[8]
+    static constexpr size_t oPst = a16(oMisc + 16 * 4);                   // u8 [8][UM + 1] run starts
+    static constexpr size_t oOrd = a16(oPst + (size_t)8 * (UM + 1));      // u8 [8][NW]
+    static constexpr size_t oUis = a16(oOrd + (size_t)8 * NW);            // u8 [8][NW]
+    static constexpr size_t oJl = a16(oUis + (size_t)8 * NW);             // u8 [8][J]
+    static constexpr size_t oFit = a16(oJl + (size_t)8 * J);              // double Ms, Ma
+    static constexpr size_t smem = a16(oFit + (size_t)(PS * PS + PA * PA) * 8);
+    static_assert(NWARP >= 8, "phase 0/2 map one warp per octant");
+    static_assert(2 * FG * P * 16 <= NW * KP * 8, "fit temporaries live in the W buffer");
+    static_assert(J <= 255 && NW <= 255, "u8 indices");
+};
+
+template <int PS, int PA>
+__global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
+                                                      double k, const double* __restrict__ Ms,
+                                                      const double* __restrict__ Ma, double2* vals_p, int* bad,
+                                                      int umax, const double2* __restrict__ zseg) {
+    using C = TcCfg<PS, PA>;
+    constexpr int P = C::P, KS = C::KS, NW = C::NW, KP = C::KP, J = C::J, UM = C::UM, NT = C::NT,
+                  NWARP = C::NWARP, R = C::R, FG = C::FG;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sV = reinterpret_cast<double2*>(smraw + C::oV);
+    double* sW = reinterpret_cast<double*>(smraw + C::oW);
+    double* sG = reinterpret_cast<double*>(smraw + C::oG);
+    int* sU = reinterpret_cast<int*>(smraw + C::oU);
+    int* sSlot = reinterpret_cast<int*>(smraw + C::oSlot);
+    int* sChild = reinterpret_cast<int*>(smraw + C::oChild);
+    int* sSeg = reinterpret_cast<int*>(smraw + C::oSeg);
+    int* sUcell = reinterpret_cast<int*>(smraw + C::oUcell);
+    int* sUn = reinterpret_cast<int*>(smraw + C::oMisc);
+    int* sNo = sUn + 8;
+    unsigned char* sPst = smraw + C::oPst;
+    unsigned char* sOrd = smraw + C::oOrd;
+    unsigned char* sUis = smraw + C::oUis;
+    unsigned char* sJl = smraw + C::oJl;
+    double* sMs = reinterpret_cast<double*>(smraw + C::oFit);
+    double* sMa = sMs + PS * PS;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t c = blockIdx.x;
+    const int s0 = LP.chunk_start[c];
+    const int s1 = (c + 1 < LP.nchunk) ? LP.chunk_start[c + 1] : (int)LP.nseg;
+    const int cnt = min(J, s1 - s0);
+
+    // ---- phase 0
+    for (int j = tid; j < J; j += NT) sSeg[j] = j < cnt ? LP.cell_seg[s0 + j] : -1;
+    for (int t = tid; t < PS * PS; t += NT) sMs[t] = Ms[t];
+    for (int t = tid; t < PA * PA; t += NT) sMa[t] = Ma[t];
+    for (int t = tid; t < J * P; t += NT) sV[t] = make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int t = tid; t < 8 * J; t += NT) {
+        const int o = t / J, j = t - o * J;
+        const int seg = sSeg[j];
+        int B = -1;
+        if (seg >= 0) {
+            B = LP.child_oct[8 * LP.seg_box[seg] + o];
+            if (B < L.b0 || B >= L.b1) B = -1;
+        }
+        sChild[t] = B;
+    }
+    __syncthreads();
+    if (warp < 8) {
+        const int o = warp;
+        int base = 0;
+        for (int j0 = 0; j0 < J; j0 += 32) {
+            const int j = j0 + lane;
+            const bool pr = j < J && sChild[o * J + j] >= 0;
+            const unsigned b = __ballot_sync(~0u, pr);
+            if (pr) sJl[o * J + base + __popc(b & lt)] = (unsigned char)j;
+            base += __popc(b);
+        }
+        if (lane == 0) sNo[o] = base;
+    }
+    __syncthreads();
+
+    // ---- phase 1: geometry of (octant, node)
+    const int cellp = LP.seg_cell[sSeg[0]];
+    const double hh = 0.5 * L.H;
+    for (int t = tid; t < 8 * NW; t += NT) {
+        const int o = t / NW, n = t - o * NW;
+        int u = INT_MAX;
+        if (n < P && sNo[o] > 0) {
+            double off[3];
+            node_off(LP, PS, PA, cellp, n, off);
+            const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
+            const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
+            const Cls cl = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+            u = (int)cell_of(L, cl);
+            // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
+            const double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
+            const double diff = num / (cl.r + rQ);
+            const double ratio = rQ / cl.r;
+            double sn, cs;
+            sincos(k * diff, &sn, &cs);
+            double* g = sG + (size_t)t * 5;
+            g[0] = cl.us;
+            g[1] = cl.ut;
+            g[2] = cl.up;
+            g[3] = ratio * cs;
+            g[4] = ratio * sn;
+        }
+        sU[t] = u;
+    }
+    __syncthreads();
+
+    // ---- phase 2: per octant (warp): distinct child cells ascending, stable node
+    // sort by cell; the nodes of cell index ui occupy sorted positions
+    // [pst[ui], pst[ui + 1])
+    if (warp < 8) {
+        const int o = warp;
+        int uv[R];
+        bool done[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int n = lane + 32 * r;
+            uv[r] = n < NW ? sU[o * NW + n] : INT_MAX;
+            done[r] = !(n < P) || uv[r] == INT_MAX;
+        }
+        int base = 0, U = 0;
+        while (true) {
+            int m = INT_MAX;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (!done[r]) m = min(m, uv[r]);
+            m = __reduce_min_sync(~0u, m);
+            if (m == INT_MAX) break;
+            if (lane == 0 && U <= UM) sPst[o * (UM + 1) + U] = (unsigned char)base;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool hit = !done[r] && uv[r] == m;
+                const unsigned b = __ballot_sync(~0u, hit);
+                if (hit) {
+                    const int pos = base + __popc(b & lt);
+                    sOrd[o * NW + pos] = (unsigned char)(lane + 32 * r);
+                    sUis[o * NW + pos] = (unsigned char)min(U, 254);
+                    done[r] = true;
+                }
+                base += __popc(b);
+            }
+            if (lane == 0 && U < UM) sUcell[o * UM + U] = m;
+            ++U;
+        }
+        if (lane == 0 && U <= UM) sPst[o * (UM + 1) + U] = (unsigned char)base;
+        for (int pos = base + lane; pos < NW; pos += 32) {
+            sOrd[o * NW + pos] = (unsigned char)pos;
+            sUis[o * NW + pos] = 0xFF;
+        }
+        if (lane == 0) sUn[o] = U;
+    }
+    __syncthreads();
+
+    // ---- phase 3: child segment slots per (octant, cell, compacted segment);
+    // -1 = no column (the B fragment then reads the zero segment)
+    for (int t = tid; t < 8 * UM * J; t += NT) {
+        const int o = t / (UM * J), rem = t - o * (UM * J), ui = rem / J, q = rem - ui * J;
+        int sl = -1;
+        if (ui < sUn[o] && sUn[o] <= umax && q < sNo[o]) {
+            const int B = sChild[o * J + sJl[o * J + q]];
+            const int64_t s64 = seg_slot(L, B, sUcell[o * UM + ui]);
+            if (s64 < 0) atomicOr(bad, 1);
+            sl = (int)s64;
+        }
+        sSlot[t] = sl;
+    }
+    __syncthreads();
+
+    // ---- phase 4: per octant, W_o then DMMA tasks
+    const int gid = lane >> 2, tig = lane & 3;
+    for (int o = 0; o < 8; ++o) {
+        const int no = sNo[o];
+        if (no == 0) continue;
+        const int U = sUn[o];
+        const double* g0 = sG + (size_t)o * NW * 5;
+        if (U <= umax) {
+            for (int t = tid; t < NW * PA; t += NT) {
+                const int pos = t / PA, cc = t - pos * PA;
+                double* wrow = sW + pos * KP;
+                if (pos < P) {
+                    const double* g = g0 + (int)sOrd[o * NW + pos] * 5;
+                    double Ts[PS], Tt[PA];
+                    cheb_T<PS>(g[0], Ts);
+                    cheb_T<PA>(g[1], Tt);
+                    const double up = g[2];
+                    double tm1 = 1.0, tp = up;
+                    if (cc == 0) tp = 1.0;
+                    for (int i = 2; i <= cc; ++i) {
+                        const double tn = fma(2.0 * up, tp, -tm1);
+                        tm1 = tp;
+                        tp = tn;
+                    }
+#pragma unroll
+                    for (int b = 0; b < PA; ++b) {
+                        const double tb = Tt[b] * tp;
+#pragma unroll
+                        for (int a = 0; a < PS; ++a) wrow[(cc * PA + b) * PS + a] = Ts[a] * tb;
+                    }
+                    if (cc == 0)
+                        for (int kk = P; kk < KP; ++kk) wrow[kk] = 0.0;
+                } else {
+                    for (int kk = cc; kk < KP; kk += PA) wrow[kk] = 0.0;
+                }
+            }
+            __syncthreads();
+            const int nst = (no + 7) >> 3;
+            const unsigned char* pst = sPst + o * (UM + 1);
+            for (int t = warp; t < nst * U; t += NWARP) {
+                const int st = t / U, ui = t - st * U;
+                // B fragments: column q = st*8 + gid, rows k = 4 ks + tig (reads one
+                // element past the segment for k = P: W is zero there; vals arrays
+                // carry a zeroed tail segment)
+                const int q = st * 8 + gid;
+                const int sl = sSlot[(o * UM + ui) * J + q];
+                const double2* cp = sl >= 0 ? vals_d + (int64_t)sl * P : zseg;
+                double2 b[KS];
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) b[ks] = __ldg(cp + 4 * ks + tig);
+                const int p0 = pst[ui], p1 = pst[ui + 1];
+                for (int tile = p0 >> 3; tile <= (p1 - 1) >> 3; ++tile) {
+                    const int pos = tile * 8 + gid;
+                    const double* wr = sW + pos * KP + tig;
+                    double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
+                    double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) {
+                        const double a = wr[4 * ks];
+                        if (ks & 1) {
+                            dmma(er0, er1, a, b[ks].x);
+                            dmma(ei0, ei1, a, b[ks].y);
+                        } else {
+                            dmma(dr0, dr1, a, b[ks].x);
+                            dmma(di0, di1, a, b[ks].y);
+                        }
+                    }
+                    if (pos >= p0 && pos < p1) {
+                        dr0 += er0;
+                        dr1 += er1;
+                        di0 += ei0;
+                        di1 += ei1;
+                        const int n = sOrd[o * NW + pos];
+                        const double rr = g0[n * 5 + 3], ri = g0[n * 5 + 4];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int qq = st * 8 + 2 * tig + h;
+                            if (qq < no) {
+                                const int j = sJl[o * J + qq];
+                                const double fr = h ? dr1 : dr0, fi = h ? di1 : di0;
+                                double2 acc = sV[j * P + n];
+                                acc.x = fma(rr, fr, fma(-ri, fi, acc.x));
+                                acc.y = fma(rr, fi, fma(ri, fr, acc.y));
+                                sV[j * P + n] = acc;
+                            }
+                        }
+                    }
+                }
+            }
+        } else {
+            // more distinct child cells than staged (near the poles): evaluate each
+            // (segment, node) from global memory; still one writer per V entry
+            for (int t = tid; t < no * P; t += NT) {
+                const int q = t / P, n = t - q * P;
+                const int j = sJl[o * J + q];
+                const int B = sChild[o * J + j];
+                const double* g = g0 + n * 5;
+                const int64_t sl = seg_slot(L, B, sU[o * NW + n]);
+                if (sl < 0) {
+                    atomicOr(bad, 1);
+                    continue;
+                }
+                const double2 F = eval_interp<PS, PA>(vals_d + sl * P, g[0], g[1], g[2]);
+                double2 acc = sV[j * P + n];
+                acc.x = fma(g[3], F.x, fma(-g[4], F.y, acc.x));
+                acc.y = fma(g[3], F.y, fma(g[4], F.x, acc.y));
+                sV[j * P + n] = acc;
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- phase 5: fused K5 fit (reading R1), groups of FG segments, three
+    // separable passes through the (now free) W buffer
+    double2* TA = reinterpret_cast<double2*>(sW);
+    double2* TB = TA + FG * P;
+    for (int j0 = 0; j0 < cnt; j0 += FG) {
+        const int nj = min(FG, cnt - j0);
+        for (int t = tid; t < nj * P; t += NT) {  // along s
+            const int jj = t / P, i = t - jj * P;
+            const int ia = i % PS, rest = i / PS;
+            const double2* v = sV + (j0 + jj) * P + rest * PS;
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int q = 0; q < PS; ++q) {
+                const double m = sMs[ia * PS + q];
+                xr = fma(m, v[q].x, xr);
+                xi = fma(m, v[q].y, xi);
+            }
+            TA[t] = make_double2(xr, xi);
+        }
+        __syncthreads();
+        for (int t = tid; t < nj * P; t += NT) {  // along theta
+            const int jj = t / P, i = t - jj * P;
+            const int ia = i % PS, ib = (i / PS) % PA, ic = i / (PS * PA);
+            const double2* v = TA + jj * P + ic * PA * PS + ia;
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int q = 0; q < PA; ++q) {
+                const double m = sMa[ib * PA + q];
+                xr = fma(m, v[q * PS].x, xr);
+                xi = fma(m, v[q * PS].y, xi);
+            }
+            TB[t] = make_double2(xr, xi);
+        }
+        __syncthreads();
+        for (int t = tid; t < nj * P; t += NT) {  // along phi
+            const int jj = t / P, i = t - jj * P;
+            const int ab = i % (PS * PA), ic = i / (PS * PA);
+            const double2* v = TB + jj * P + ab;
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int q = 0; q < PA; ++q) {
+                const double m = sMa[ic * PA + q];
+                xr = fma(m, v[q * PS * PA].x, xr);
+                xi = fma(m, v[q * PS * PA].y, xi);
+            }
+            vals_p[(int64_t)sSeg[j0 + jj] * P + i] = make_double2(xr, xi);
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------- dispatch
 template <int PS, int PA>
 struct Kern {
@@ -892,6 +1272,21 @@ struct Kern {
     // returns true if the kernel also produced the Chebyshev coefficients (fused K5)
     static bool upward(dim3 g, cudaStream_t st, const LevelParams& L, const LevelParams& LP, const ifgf_plan_s* p,
                        const double2* vd, double2* vp, int* bad) {
+        if constexpr (PS > 0 && PS * PA * PA <= 80) {
+            if (LP.up_tc && LP.nchunk > 0) {
+                using Cfg = TcCfg<PS, PA>;
+                static bool attr = false;
+                if (!attr) {
+                    IFGF_CUDA(cudaFuncSetAttribute(k_upward_tc<PS, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)Cfg::smem));
+                    attr = true;
+                }
+                k_upward_tc<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(L, LP, vd, p->k, p->cheb_Ms,
+                                                                                       p->cheb_Ma, vp, bad, std::min(Cfg::UM, p->tc_umax),
+                                                                                       p->zseg);
+                return true;
+            }
+        }
         if constexpr (PS > 0 && PS * PA * PA <= 80) {
             // FP64 tensor-core kernel: opt-in (mode 4) until it beats the staged DFMA kernel
             if (p->legacy_upward == 4 && LP.nchunk > 0) {

@@ -84,9 +84,14 @@ struct LevelParams {  // passed by value to kernels
     const int* cell_seg;
     const int* chunk_start;
     int64_t nchunk;
+    // K7 kernel of the level when it is the PARENT level: 0 = staged DFMA kernel
+    // (chunks of <= kChunk segments), 1 = FP64 tensor-core kernel (chunks of
+    // <= kChunkTC segments); chosen at plan time from the segments per cell.
+    int up_tc;
 };
 
 constexpr int kChunk = 16;
+constexpr int kChunkTC = 64;
 
 struct LevelHost {
     LevelParams p{};
@@ -124,7 +129,8 @@ struct ifgf_plan_s {
     // apply scratch
     double2* a_sorted = nullptr;
     double2* out_sorted = nullptr;
-    double2* vals[2] = {nullptr, nullptr};  // ping-pong by level parity
+    double2* vals[2] = {nullptr, nullptr};  // ping-pong by level parity (+1 zeroed tail segment)
+    double2* zseg = nullptr;                // P + 4 zeros: the TC K7's absent-column operand
     int64_t vals_cap[2] = {0, 0};
     double2* host_stage_dev_in = nullptr;   // ifgf_apply_host buffers
     double2* host_stage_dev_out = nullptr;
@@ -141,7 +147,8 @@ struct ifgf_plan_s {
     };
     std::vector<PendingEv> pending;
     int* dev_bad = nullptr;  // device flag: apply-time invariant violation (EINTERNAL)
-    int legacy_upward = 0;   // env IFGF_LEGACY_UPWARD=1: per-evaluation-geometry K7 (A/B testing)
+    int legacy_upward = 0;   // env IFGF_LEGACY_UPWARD: K7 variant override (A/B testing, tests)
+    int tc_umax = 1 << 30;   // env IFGF_TC_UMAX: cap on staged child cells in the TC K7 (tests the fallback)
     int64_t device_bytes = 0;
     std::vector<void*> allocs;  // every cudaMalloc of the plan
 };

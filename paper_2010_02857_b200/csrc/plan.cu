@@ -858,8 +858,19 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         IFGF_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, rs, rsm, MaxOp(), (int)ns, st));
         S.release(tmp);
         int* flag = rs;  // reuse
-        k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, kChunk, flag);
         int* incl = S.get<int>(ns);
+        // runs of equal (tile, cell): their mean length picks the K7 kernel of this
+        // parent level (tensor-core GEMM when many segments share a cell)
+        k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, 0x7fffffff, flag);
+        inclusive_scan(S, flag, incl, ns, st);
+        const int64_t nrun = d2h_one(incl + ns - 1, st);
+        const double per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
+        int tc = per_run >= 24.0 ? 1 : 0;
+        if (p->legacy_upward >= 1 && p->legacy_upward <= 4) tc = 0;  // legacy A/B variants: 16-chunks
+        if (p->legacy_upward == 5) tc = 1;                           // force the tensor-core kernel
+        if (P > 80) tc = 0;  // TC kernel shared memory is sized for P <= 80 (P_s, P_ang) = (3, 5)
+        L.p.up_tc = tc;
+        k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, tc ? kChunkTC : kChunk, flag);
         inclusive_scan(S, flag, incl, ns, st);
         int64_t nch = d2h_one(incl + ns - 1, st);
         L.chunk_start = dev_alloc<int>(p, nch);
@@ -912,6 +923,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             s.cousin_evals[d] = d >= 3 ? (int64_t)h[4 * d] : 0;
             s.upward_evals[d] = d >= 4 ? (int64_t)h[4 * d + 1] : 0;
             s.segment_bytes[d] = 16LL * P * p->lev[d].p.nseg;
+            s.upward_kernel[d] = (d >= 4 && p->lev[d - 1].p.nseg > 0) ? p->lev[d - 1].p.up_tc : -1;
         }
     }
 
@@ -923,8 +935,13 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         for (int d = 3; d <= D; ++d)
             if ((d & 1) == par) mx = std::max(mx, p->lev[d].p.nseg);
         p->vals_cap[par] = mx * P;
-        p->vals[par] = dev_alloc<double2>(p, mx * P);
+        // one extra zeroed segment: the TC K7 reads k = 4*ceil(P/4)-1 >= P past a
+        // segment's end (times a zero weight), so that memory must be finite
+        p->vals[par] = dev_alloc<double2>(p, (mx + 1) * P);
+        IFGF_CUDA(cudaMemsetAsync(p->vals[par], 0, sizeof(double2) * (size_t)(mx + 1) * P, st));
     }
+    p->zseg = dev_alloc<double2>(p, P + 4);
+    IFGF_CUDA(cudaMemsetAsync(p->zseg, 0, sizeof(double2) * (size_t)(P + 4), st));
     IFGF_CUDA(cudaStreamSynchronize(st));
     p->stats.plan_device_bytes = p->device_bytes;
     p->stats.plan_ms =

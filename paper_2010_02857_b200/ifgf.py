@@ -52,6 +52,7 @@ class IfgfStats(ctypes.Structure):
         ("cousin_evals", ctypes.c_int64 * _L1), ("upward_evals", ctypes.c_int64 * _L1),
         ("segment_bytes", ctypes.c_int64 * _L1),
         ("plan_device_bytes", ctypes.c_int64), ("plan_ms", ctypes.c_double),
+        ("upward_kernel", ctypes.c_int * _L1),
     ]
 
 
@@ -209,6 +210,7 @@ class Plan:
             cousin_evals={d: s.cousin_evals[d] for d in lv}, upward_evals={d: s.upward_evals[d] for d in lv},
             segment_bytes={d: s.segment_bytes[d] for d in lv},
             plan_device_bytes=s.plan_device_bytes, plan_ms=s.plan_ms,
+            upward_kernel={d: s.upward_kernel[d] for d in lv},
         )
 
     def level_segments(self, d: int) -> np.ndarray:

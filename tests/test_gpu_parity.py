@@ -204,6 +204,20 @@ def test_multirank_emulation_one_gpu(ifgf):
         assert oracle.rel_l2(acc, full) < 1e-13, R
 
 
+def test_default_kernel_choice_tc_and_staged(ifgf):
+    """At the default settings a lambda/4-leaf sphere uses the FP64 tensor-core
+    K7 on its fine levels and the staged DFMA K7 on the coarse ones; both match
+    the oracle."""
+    n, k, D = 60000, 8 * math.pi, 6
+    pts = inputs.fibonacci_sphere(n)
+    a = inputs.densities(n, seed=5)
+    _, got, st = run_gpu(ifgf, pts, a, k, D)
+    kern = st["upward_kernel"]
+    assert kern[D] == 1 and kern[4] == 0, kern
+    ref = oracle.OraclePlan(pts, k, D, 3, 5).apply(a)
+    assert oracle.rel_l2(got, ref) <= PARITY
+
+
 # ------------------------------------------------------------ larger configs
 @pytest.mark.slow
 def test_cfg2_parity(ifgf):
@@ -220,12 +234,19 @@ def test_cfg2_parity(ifgf):
     assert oracle.rel_l2(got[tg], exact) <= 1.1 * oracle.rel_l2(ref[tg], exact)
 
 
-@pytest.mark.parametrize("mode", ["1", "2", "3", "4"])
-def test_upward_kernel_variants(ifgf, mode, monkeypatch):
+@pytest.mark.parametrize("mode,umax", [("1", None), ("2", None), ("3", None), ("4", None), ("5", None),
+                                       ("5", "1"), ("5", "0")])
+def test_upward_kernel_variants(ifgf, mode, umax, monkeypatch):
     """Every K7 variant (1 per-evaluation geometry, 2 cell-grouped, 3 cell-grouped
-    + shared-memory staged, 4 FP64 tensor-core DMMA) matches the oracle; the
-    default (0) picks DMMA for dense chunks and the staged kernel otherwise."""
+    + shared-memory staged, 4 FP64 tensor-core DMMA on 16-chunks, 5 the FP64
+    tensor-core GEMM kernel on 64-chunks at every level) matches the oracle.
+    IFGF_TC_UMAX caps the child cells the TC kernel stages per octant, so that its
+    per-node fallback (taken near the poles) is exercised too.  The default (0)
+    picks the TC kernel where many segments share a cell, the staged kernel
+    elsewhere."""
     monkeypatch.setenv("IFGF_LEGACY_UPWARD", mode)
+    if umax is not None:
+        monkeypatch.setenv("IFGF_TC_UMAX", umax)
     n = 20000
     pts = inputs.fibonacci_sphere(n, (1.0, 1.0, 0.5))
     a = inputs.densities(n, seed=21)
