@@ -6,6 +6,7 @@
 // Every output has exactly one writer (target-major K3/K6, parent-node-major
 // K7): no atomics on values, deterministic results.
 #include <climits>
+#include <cstdio>
 #include <cmath>
 
 #include "ifgf_internal.cuh"
@@ -20,6 +21,16 @@ constexpr double kInv4Pi = 0.079577471545947667884;  // 1/(4 pi)
 inline int nblk(int64_t n, int tpb = TPB) {
     int64_t b = (n + tpb - 1) / tpb;
     return (int)(b < 1 ? 1 : b);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 __global__ void k_permute(const double2* __restrict__ in, const int* __restrict__ perm, int64_t n, double2* out) {
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(TPB) k_cousin(LevelParams L, const double* __r
         }
         double2 F = interp<PS, PA>(vals + slot * P, Ps, Pa, c.us, c.ut, c.up);
         double sn, cs;
-        sincos(k * c.r, &sn, &cs);
+        fm::sincos(k * c.r, &sn, &cs);
         double w = kInv4Pi / c.r;
         double gr = cs * w, gi = sn * w;
         ar = fma(gr, F.x, fma(-gi, F.y, ar));
@@ -241,6 +252,107 @@ __global__ void __launch_bounds__(TPB) k_cousin(LevelParams L, const double* __r
     }
     double2 o = out[l];
     out[l] = make_double2(o.x + ar, o.y + ai);
+}
+
+// K6, warp-staged and pipelined: target-major as k_cousin (one warp per
+// (target box T, 32 targets); the cousin source box B is warp-uniform).  For
+// each B the warp finds the distinct (B, cell) segments its targets fall in
+// (<= SMAX, leader election with ballots) and copies their coefficient vectors
+// into the warp's shared-memory slots with cp.async; every lane then contracts
+// from its own slot at the same time (distinct slots sit in disjoint banks), so
+// neither the DFMA work nor the loads serialise over distinct segments.  The
+// classification of box e+1 and its copies are issued before box e is
+// contracted (double-buffered slots), hiding the global-memory latency.
+template <int PS, int PA>
+struct CousinEv {
+    int64_t slot;  // segment slot (-1: none)
+    int bi;        // shared-memory slot index, -1 if beyond SMAX (global fallback)
+    double gr, gi, up, Ts[PS], Tt[PA];
+};
+
+template <int PS, int PA>
+__global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const double* __restrict__ px,
+                                                   const double* __restrict__ py, const double* __restrict__ pz,
+                                                   const double2* __restrict__ vals, double k, double2* out,
+                                                   int* bad) {
+    constexpr int P = PS * PA * PA;
+    constexpr int SMAX = P <= 80 ? 4 : 2;  // static shared memory <= 48 KB per block
+    constexpr int SP = P + 2;  // slot stride (double2): 4 slots -> disjoint banks for 16-byte reads
+    __shared__ __align__(16) double2 sbuf[TPB / 32][2][SMAX][SP];
+    const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (item >= L.nwitems) return;  // warp-uniform
+    const int2 it = L.witems[item];
+    const int T = it.x, l = it.y + lane;
+    const bool active = l < L.box_start[T + 1];
+    double x = 0.0, y = 0.0, z = 0.0;
+    if (active) {
+        x = px[l];
+        y = py[l];
+        z = pz[l];
+    }
+    auto prep = [&](int e, CousinEv<PS, PA>& v, int buf) {
+        v.slot = -1;
+        v.bi = -1;
+        const int B = L.cou_idx[e];
+        if (B >= L.b0 && B < L.b1) {
+            const double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
+                         cz = box_centre(L, L.box_ijk[3 * B + 2], 2);
+            if (active) {
+                const Cls c = classify(L, __dsub_rn(x, cx), __dsub_rn(y, cy), __dsub_rn(z, cz));
+                v.slot = seg_slot(L, B, cell_of(L, c));
+                if (v.slot < 0) atomicOr(bad, 1);
+                double sn, cs;
+                fm::sincos(k * c.r, &sn, &cs);
+                const double wr = kInv4Pi / c.r;
+                v.gr = cs * wr;
+                v.gi = sn * wr;
+                cheb_T<PS>(c.us, v.Ts);
+                cheb_T<PA>(c.ut, v.Tt);
+                v.up = c.up;
+            }
+            unsigned pend = __ballot_sync(~0u, v.slot >= 0);
+            int nd = 0;
+            while (pend && nd < SMAX) {
+                const int leader = __ffs(pend) - 1;
+                const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
+                const double2* src = vals + s0 * P;
+                double2* dst = &sbuf[w][buf][nd][0];
+                for (int i = lane; i < P; i += 32) cp_async16(dst + i, src + i);
+                const bool mine = v.slot == s0;
+                if (mine) v.bi = nd;
+                pend &= ~__ballot_sync(~0u, mine);
+                ++nd;
+            }
+        }
+        cp_async_commit();
+    };
+    double ar = 0.0, ai = 0.0;
+    const int e0 = L.cou_off[T], e1 = L.cou_off[T + 1];
+    CousinEv<PS, PA> cur, nxt;
+    if (e0 < e1) prep(e0, cur, 0);
+    for (int e = e0; e < e1; ++e) {
+        if (e + 1 < e1) {
+            prep(e + 1, nxt, (e + 1 - e0) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        if (cur.slot >= 0) {
+            const double2 F = cur.bi >= 0
+                                  ? contract_sm_lr<PS, PA>(&sbuf[w][(e - e0) & 1][cur.bi][0], cur.Ts, cur.Tt, cur.up)
+                                  : contract_sm_lr<PS, PA>(vals + cur.slot * P, cur.Ts, cur.Tt, cur.up);
+            ar = fma(cur.gr, F.x, fma(-cur.gi, F.y, ar));
+            ai = fma(cur.gr, F.y, fma(cur.gi, F.x, ai));
+        }
+        __syncwarp();  // slot buffer (e & 1) is refilled by prep(e + 2)
+        cur = nxt;
+    }
+    if (active) {
+        const double2 o = out[l];
+        out[l] = make_double2(o.x + ar, o.y + ai);
+    }
 }
 
 // K7: V_Q[gamma', y] = sum over owned children B of Q of
@@ -276,7 +388,7 @@ __global__ void __launch_bounds__(TPB) k_upward(LevelParams L, LevelParams LP, c
         double diff = num / (c.r + rQ);
         double ratio = rQ / c.r;
         double sn, cs;
-        sincos(k * diff, &sn, &cs);
+        fm::sincos(k * diff, &sn, &cs);
         double gr = ratio * cs, gi = ratio * sn;
         ar = fma(gr, F.x, fma(-gi, F.y, ar));
         ai = fma(gr, F.y, fma(gi, F.x, ai));
@@ -336,7 +448,7 @@ __global__ void __launch_bounds__(128, 4) k_upward_g(LevelParams L, LevelParams 
         double diff = num / (cl.r + rQ);
         double ratio = rQ / cl.r;
         double sn, cs;
-        sincos(k * diff, &sn, &cs);
+        fm::sincos(k * diff, &sn, &cs);
         const double rr = ratio * cs, ri = ratio * sn;
         double Ts[PS], Tt[PA];
         cheb_T<PS>(cl.us, Ts);
@@ -368,61 +480,6 @@ __global__ void __launch_bounds__(128, 4) k_upward_g(LevelParams L, LevelParams 
 // segments) and every thread contracts from shared memory.  This turns the
 // per-evaluation chain of dependent global loads into one bulk, fully
 // overlapped copy per (segment, octant).
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-// Tensor contraction from shared memory (same order as contract()).
-template <int PS, int PA>
-__device__ __forceinline__ double2 contract_sm(const double2* C, const double* Ts, const double* Tt, double up) {
-    double wr[PA * PS], wi[PA * PS];
-#pragma unroll
-    for (int i = 0; i < PA * PS; ++i) {
-        double2 v = C[i];
-        wr[i] = v.x;
-        wi[i] = v.y;
-    }
-    double tm1 = 1.0, t = up;
-    const double u2 = 2.0 * up;
-#pragma unroll
-    for (int c = 1; c < PA; ++c) {
-#pragma unroll
-        for (int i = 0; i < PA * PS; ++i) {
-            double2 v = C[c * PA * PS + i];
-            wr[i] = fma(t, v.x, wr[i]);
-            wi[i] = fma(t, v.y, wi[i]);
-        }
-        const double tn = fma(u2, t, -tm1);
-        tm1 = t;
-        t = tn;
-    }
-    double xr[PS], xi[PS];
-#pragma unroll
-    for (int a = 0; a < PS; ++a) {
-        xr[a] = wr[a];
-        xi[a] = wi[a];
-    }
-#pragma unroll
-    for (int b = 1; b < PA; ++b)
-#pragma unroll
-        for (int a = 0; a < PS; ++a) {
-            xr[a] = fma(Tt[b], wr[b * PS + a], xr[a]);
-            xi[a] = fma(Tt[b], wi[b * PS + a], xi[a]);
-        }
-    double fr = xr[0], fi = xi[0];
-#pragma unroll
-    for (int a = 1; a < PS; ++a) {
-        fr = fma(Ts[a], xr[a], fr);
-        fi = fma(Ts[a], xi[a], fi);
-    }
-    return make_double2(fr, fi);
-}
 
 template <int PS, int PA>
 struct StagedCfg {
@@ -491,7 +548,7 @@ __global__ void __launch_bounds__(128, 3) k_upward_s(LevelParams L, LevelParams 
             double diff = num / (cl.r + rQ);
             double ratio = rQ / cl.r;
             double sn, cs;
-            sincos(k * diff, &sn, &cs);
+            fm::sincos(k * diff, &sn, &cs);
             rr = ratio * cs;
             ri = ratio * sn;
             cheb_T<PS>(cl.us, Ts);
@@ -726,7 +783,7 @@ __global__ void __launch_bounds__(128, 2) k_upward_mma(LevelParams L, LevelParam
             double diff = num / (cl.r + rQ);
             double ratio = rQ / cl.r;
             double sn, cs;
-            sincos(k * diff, &sn, &cs);
+            fm::sincos(k * diff, &sn, &cs);
             sh_rec[n] = make_double2(ratio * cs, ratio * sn);
             cheb_T<PS>(cl.us, Ts);
             cheb_T<PA>(cl.ut, Tt);
@@ -919,7 +976,7 @@ struct TcCfg {
     static constexpr int KP = ((4 * KS) % 16 == 4 || (4 * KS) % 16 == 12) ? 4 * KS : 4 * KS + 4;
     static constexpr int J = kChunkTC;
     static constexpr int UM = 8;              // distinct child cells per octant with staged slots
-    static constexpr int NT = 384;
+    static constexpr int NT = 256;
     static constexpr int NWARP = NT / 32;
     static constexpr int R = (NW + 31) / 32;
     static constexpr int FG = 16;             // fit group (segments)
@@ -945,11 +1002,22 @@ struct TcCfg {
 };
 
 template <int PS, int PA>
-__global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
+__global__ void __launch_bounds__(256, 1) k_upward_tc(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
                                                       double k, const double* __restrict__ Ms,
                                                       const double* __restrict__ Ma, double2* vals_p, int* bad,
-                                                      int umax, const double2* __restrict__ zseg) {
+                                                      int umax, const double2* __restrict__ zseg,
+                                                      unsigned long long* __restrict__ phase_clk) {
     using C = TcCfg<PS, PA>;
+    // optional per-phase clock accounting (env IFGF_PHASE_PROF): thread 0 adds the
+    // cycles since the previous mark to phase_clk[i]
+    long long t_mark = clock64();
+    auto mark = [&](int i) {
+        if (phase_clk && threadIdx.x == 0) {
+            const long long t = clock64();
+            atomicAdd(phase_clk + i, (unsigned long long)(t - t_mark));
+            t_mark = t;
+        }
+    };
     constexpr int P = C::P, KS = C::KS, NW = C::NW, KP = C::KP, J = C::J, UM = C::UM, NT = C::NT,
                   NWARP = C::NWARP, R = C::R, FG = C::FG;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -1007,6 +1075,7 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
         if (lane == 0) sNo[o] = base;
     }
     __syncthreads();
+    mark(0);
 
     // ---- phase 1: geometry of (octant, node)
     const int cellp = LP.seg_cell[sSeg[0]];
@@ -1026,7 +1095,7 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
             const double diff = num / (cl.r + rQ);
             const double ratio = rQ / cl.r;
             double sn, cs;
-            sincos(k * diff, &sn, &cs);
+            fm::sincos(k * diff, &sn, &cs);
             double* g = sG + (size_t)t * 5;
             g[0] = cl.us;
             g[1] = cl.ut;
@@ -1037,6 +1106,7 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
         sU[t] = u;
     }
     __syncthreads();
+    mark(1);
 
     // ---- phase 2: per octant (warp): distinct child cells ascending, stable node
     // sort by cell; the nodes of cell index ui occupy sorted positions
@@ -1083,6 +1153,7 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
         if (lane == 0) sUn[o] = U;
     }
     __syncthreads();
+    mark(2);
 
     // ---- phase 3: child segment slots per (octant, cell, compacted segment);
     // -1 = no column (the B fragment then reads the zero segment)
@@ -1098,6 +1169,7 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
         sSlot[t] = sl;
     }
     __syncthreads();
+    mark(3);
 
     // ---- phase 4: per octant, W_o then DMMA tasks
     const int gid = lane >> 2, tig = lane & 3;
@@ -1136,21 +1208,57 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
                 }
             }
             __syncthreads();
+            mark(4);
+            // Tasks (segment tile st, child cell ui, node tile) enumerated st-major;
+            // warp w takes the contiguous range [w T / NWARP, (w+1) T / NWARP), so
+            // consecutive tasks mostly share (st, ui) and its B fragments stay in
+            // registers; the next group's B fragments are prefetched while the
+            // current group's node tiles run (register double buffer).
             const int nst = (no + 7) >> 3;
             const unsigned char* pst = sPst + o * (UM + 1);
-            for (int t = warp; t < nst * U; t += NWARP) {
-                const int st = t / U, ui = t - st * U;
-                // B fragments: column q = st*8 + gid, rows k = 4 ks + tig (reads one
-                // element past the segment for k = P: W is zero there; vals arrays
-                // carry a zeroed tail segment)
-                const int q = st * 8 + gid;
-                const int sl = sSlot[(o * UM + ui) * J + q];
+            int S = 0;
+            for (int u = 0; u < U; ++u) S += ((pst[u + 1] - 1) >> 3) - (pst[u] >> 3) + 1;
+            const int T = nst * S;
+            const int tau0 = (int)((int64_t)warp * T / NWARP), tau1 = (int)((int64_t)(warp + 1) * T / NWARP);
+            // decode task tau -> (st, ui, first tile of ui, tiles left in the group)
+            auto decode = [&](int tau, int& st, int& ui, int& tl0, int& off) {
+                st = tau / S;
+                int r = tau - st * S;
+                ui = 0;
+                while (true) {
+                    const int a0 = pst[ui] >> 3, n_t = ((pst[ui + 1] - 1) >> 3) - a0 + 1;
+                    if (r < n_t) {
+                        tl0 = a0;
+                        off = r;
+                        break;
+                    }
+                    r -= n_t;
+                    ++ui;
+                }
+            };
+            auto load_b = [&](int st, int ui, double2* bb) {
+                const int sl = sSlot[(o * UM + ui) * J + st * 8 + gid];
                 const double2* cp = sl >= 0 ? vals_d + (int64_t)sl * P : zseg;
-                double2 b[KS];
 #pragma unroll
-                for (int ks = 0; ks < KS; ++ks) b[ks] = __ldg(cp + 4 * ks + tig);
+                for (int ks = 0; ks < KS; ++ks) bb[ks] = __ldg(cp + 4 * ks + tig);
+            };
+            double2 bc[KS], bn[KS];
+            int tau = tau0;
+            int st = 0, ui = 0, tl0 = 0, off = 0;
+            if (tau < tau1) {
+                decode(tau, st, ui, tl0, off);
+                load_b(st, ui, bc);
+            }
+            while (tau < tau1) {
+                const int ntl = ((pst[ui + 1] - 1) >> 3) - tl0 + 1;
+                const int gend = min(tau1, tau + (ntl - off));  // end of this (st, ui) group
+                int st2 = 0, ui2 = 0, tl02 = 0, off2 = 0;
+                if (gend < tau1) {
+                    decode(gend, st2, ui2, tl02, off2);
+                    load_b(st2, ui2, bn);
+                }
                 const int p0 = pst[ui], p1 = pst[ui + 1];
-                for (int tile = p0 >> 3; tile <= (p1 - 1) >> 3; ++tile) {
+                for (int tile = tl0 + off; tile < tl0 + off + (gend - tau); ++tile) {
                     const int pos = tile * 8 + gid;
                     const double* wr = sW + pos * KP + tig;
                     double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
@@ -1159,11 +1267,11 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
                     for (int ks = 0; ks < KS; ++ks) {
                         const double a = wr[4 * ks];
                         if (ks & 1) {
-                            dmma(er0, er1, a, b[ks].x);
-                            dmma(ei0, ei1, a, b[ks].y);
+                            dmma(er0, er1, a, bc[ks].x);
+                            dmma(ei0, ei1, a, bc[ks].y);
                         } else {
-                            dmma(dr0, dr1, a, b[ks].x);
-                            dmma(di0, di1, a, b[ks].y);
+                            dmma(dr0, dr1, a, bc[ks].x);
+                            dmma(di0, di1, a, bc[ks].y);
                         }
                     }
                     if (pos >= p0 && pos < p1) {
@@ -1187,6 +1295,15 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
                         }
                     }
                 }
+                tau = gend;
+                if (tau < tau1) {
+                    st = st2;
+                    ui = ui2;
+                    tl0 = tl02;
+                    off = off2;
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) bc[ks] = bn[ks];
+                }
             }
         } else {
             // more distinct child cells than staged (near the poles): evaluate each
@@ -1209,6 +1326,7 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
             }
         }
         __syncthreads();
+        mark(5);
     }
 
     // ---- phase 5: fused K5 fit (reading R1), groups of FG segments, three
@@ -1260,6 +1378,7 @@ __global__ void __launch_bounds__(384, 1) k_upward_tc(LevelParams L, LevelParams
         }
         __syncthreads();
     }
+    mark(6);
 }
 
 // ------------------------------------------------------------- dispatch
@@ -1267,6 +1386,12 @@ template <int PS, int PA>
 struct Kern {
     static void cousin(dim3 g, cudaStream_t st, const LevelParams& L, const ifgf_plan_s* p, const double2* v,
                        double2* out, int* bad) {
+        if constexpr (PS > 0) {
+            if (!p->legacy_cousin) {
+                k_cousin_ws<PS, PA><<<g, TPB, 0, st>>>(L, p->px, p->py, p->pz, v, p->k, out, bad);
+                return;
+            }
+        }
         k_cousin<PS, PA><<<g, TPB, 0, st>>>(L, p->px, p->py, p->pz, v, p->k, p->Ps, p->Pa, out, bad);
     }
     // returns true if the kernel also produced the Chebyshev coefficients (fused K5)
@@ -1283,7 +1408,7 @@ struct Kern {
                 }
                 k_upward_tc<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(L, LP, vd, p->k, p->cheb_Ms,
                                                                                        p->cheb_Ma, vp, bad, std::min(Cfg::UM, p->tc_umax),
-                                                                                       p->zseg);
+                                                                                       p->zseg, p->phase_clk);
                 return true;
             }
         }
@@ -1434,6 +1559,17 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
         } else {
             have = false;
         }
+    }
+    if (p->phase_clk) {
+        unsigned long long h[16];
+        IFGF_CUDA(cudaMemcpyAsync(h, p->phase_clk, sizeof(h), cudaMemcpyDeviceToHost, st));
+        IFGF_CUDA(cudaStreamSynchronize(st));
+        IFGF_CUDA(cudaMemsetAsync(p->phase_clk, 0, sizeof(h), st));
+        double tot = 0;
+        for (int i = 0; i < 7; ++i) tot += (double)h[i];
+        fprintf(stderr, "[ifgf] TC K7 phase clocks (block-thread-0 sums, %% of total %.3g):", tot);
+        for (int i = 0; i < 7; ++i) fprintf(stderr, " p%d=%.1f%%", i, 100.0 * (double)h[i] / (tot > 0 ? tot : 1));
+        fprintf(stderr, "\n");
     }
     {
         Prof pr(p, st, 6);

@@ -235,6 +235,7 @@ ifgf_status ifgf_plan(const double* points, int64_t n, double k, int levels, int
     p->P = P_s * P_ang * P_ang;
     if (const char* e = std::getenv("IFGF_LEGACY_UPWARD")) p->legacy_upward = std::atoi(e);
     if (const char* e = std::getenv("IFGF_TC_UMAX")) p->tc_umax = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("IFGF_LEGACY_COUSIN")) p->legacy_cousin = std::atoi(e);
     p->stage_mask = o.stage_mask ? o.stage_mask : IFGF_STAGE_ALL;
     p->rank = o.nranks > 1 ? o.rank : 0;
     p->nranks = o.nranks > 1 ? o.nranks : 1;
@@ -242,6 +243,10 @@ ifgf_status ifgf_plan(const double* points, int64_t n, double k, int levels, int
         p->dev_bad = ifgf::dev_alloc<int>(p, 1);
         IFGF_CUDA(cudaMemset(p->dev_bad, 0, sizeof(int)));
         ifgf::build_plan(p, points, o);
+        if (std::getenv("IFGF_PHASE_PROF")) {
+            p->phase_clk = ifgf::dev_alloc<unsigned long long>(p, 16);
+            IFGF_CUDA(cudaMemset(p->phase_clk, 0, 16 * sizeof(unsigned long long)));
+        }
     });
     if (st != IFGF_OK) {
         free_plan(p);

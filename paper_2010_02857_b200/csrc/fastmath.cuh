@@ -1,0 +1,105 @@
+// fastmath.cuh -- lean FP64 atan2 and sincos for the IFGF kernels.
+//
+// The classification contract makes every DISCRETE decision from
+// IEEE-rounded + - * / sqrt against host-libm tables; the transcendental
+// functions below only produce VALUES (local interpolation coordinates, phases),
+// where the paper's method tolerates ulp-level differences (reading R12).  CUDA's
+// libdevice atan2 / sincos spend ~125 / ~80 instructions on special cases (inf,
+// NaN, denormals, Payne-Hanek reduction) that cannot occur here; these versions
+// are branch-light polynomials:
+//   fm_atan2: octant reduction to |t| <= tan(pi/8) with ONE division, then an odd
+//             polynomial of degree 23 (near-minimax, Chebyshev-interpolated in
+//             high precision; rel. error < 5e-18 before rounding).
+//   fm_sincos: Cody-Waite reduction by pi/2 with a 3-part constant (FMA), then
+//             degree-15 / degree-16 polynomials on |r| <= pi/4 (abs. error < 1e-17
+//             before rounding); |x| >= 2^30 falls back to libdevice sincos.
+// Coefficients were generated with mpmath (60 digits) by Chebyshev interpolation
+// of (atan(t) - t)/t^3, (sin(r) - r)/r^3 and (cos(r) - 1 + r^2/2)/r^4 in t^2 / r^2.
+// Both functions compile for host and device so that the CPU unit test
+// (tests/test_fastmath_cpu.py) can check them against mpmath without a GPU.
+#pragma once
+
+#include <cmath>
+
+#ifdef __CUDACC__
+#define IFGF_HD __host__ __device__ __forceinline__
+#else
+#define IFGF_HD inline
+#endif
+
+namespace ifgf {
+namespace fm {
+
+constexpr double kTanPi8 = 0.41421356237309503;
+constexpr double kPi4 = 0.7853981633974483, kPi4Lo = 3.061616997868383e-17;
+constexpr double kPi2 = 1.5707963267948966, kPi2Lo = 6.123233995736766e-17;
+constexpr double kPiHi = 3.141592653589793, kPiLo = 1.2246467991473532e-16;
+constexpr double k2OverPi = 0.6366197723675814;
+constexpr double kPio2_1 = 1.5707963267948966, kPio2_2 = 6.123233995736766e-17, kPio2_3 = -1.4973849048591698e-33;
+
+// Polynomial coefficients: see the header comment.
+
+// atan2(y, x) in (-pi, pi]; (x, y) != (0, 0).
+IFGF_HD double atan2(double y, double x) {
+    const double ax = std::fabs(x), ay = std::fabs(y);
+    const double mx = std::fmax(ax, ay), mn = std::fmin(ax, ay);
+    const bool big = mn > kTanPi8 * mx;  // reduce via atan(t) = pi/4 + atan((t-1)/(t+1))
+    const double t = (big ? mn - mx : mn) / (big ? mn + mx : mx);
+    const double s = t * t;
+    double q = -0.019176887119062258989;
+    q = std::fma(q, s, 0.039231658295587191303);
+    q = std::fma(q, s, -0.050854497379402598613);
+    q = std::fma(q, s, 0.058581489128022098816);
+    q = std::fma(q, s, -0.066645114473819480001);
+    q = std::fma(q, s, 0.076921831908260865637);
+    q = std::fma(q, s, -0.090909045781239018905);
+    q = std::fma(q, s, 0.11111111015256361727);
+    q = std::fma(q, s, -0.14285714284666542922);
+    q = std::fma(q, s, 0.19999999999995520678);
+    q = std::fma(q, s, -0.3333333333333333016);
+    double r = std::fma(t * s, q, t);  // atan(mn / mx) (- pi/4 if big)
+    if (big) r = kPi4 + (r + kPi4Lo);
+    if (ay > ax) r = kPi2 - (r - kPi2Lo);
+    if (x < 0.0) r = kPiHi - (r - kPiLo);
+    return std::copysign(r, y);
+}
+
+// sin and cos of x (any finite x).
+IFGF_HD void sincos(double x, double* sp, double* cp) {
+    const double q = std::rint(x * k2OverPi);
+    if (!(std::fabs(q) < 1073741824.0)) {  // |x| >~ 1.7e9 (or non-finite): full reduction
+#ifdef __CUDA_ARCH__
+        ::sincos(x, sp, cp);
+#else
+        *sp = std::sin(x);
+        *cp = std::cos(x);
+#endif
+        return;
+    }
+    double r = std::fma(-q, kPio2_1, x);
+    r = std::fma(-q, kPio2_2, r);
+    r = std::fma(-q, kPio2_3, r);
+    const double s = r * r;
+    double ps = -7.5866970028175042058e-13;
+    ps = std::fma(ps, s, 1.6058531617037151954e-10);
+    ps = std::fma(ps, s, -2.5052106232435281095e-8);
+    ps = std::fma(ps, s, 2.7557319219339131119e-6);
+    ps = std::fma(ps, s, -0.00019841269841265064901);
+    ps = std::fma(ps, s, 0.0083333333333333314921);
+    ps = std::fma(ps, s, -0.16666666666666666666);
+    double pc = -1.1382632258093614476e-11;
+    pc = std::fma(pc, s, 2.0876146266079308857e-9);
+    pc = std::fma(pc, s, -2.7557317271718642711e-7);
+    pc = std::fma(pc, s, 0.000024801587298765666432);
+    pc = std::fma(pc, s, -0.0013888888888887397222);
+    pc = std::fma(pc, s, 0.041666666666666665389);
+    const double sn = std::fma(r * s, ps, r);
+    const double cs = std::fma(s * s, pc, std::fma(-0.5, s, 1.0));
+    const int iq = (int)(long long)q & 3;
+    const double a = (iq & 1) ? cs : sn, b = (iq & 1) ? sn : cs;
+    *sp = (iq & 2) ? -a : a;
+    *cp = ((iq + 1) & 2) ? -b : b;
+}
+
+}  // namespace fm
+}  // namespace ifgf

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/ifgf.h"
+#include "fastmath.cuh"
 
 namespace ifgf {
 
@@ -46,6 +47,7 @@ struct LevelParams {  // passed by value to kernels
     int64_t ncell;       // 2 * ns * nC^2
     int64_t W;           // 64-bit bitmap words per box
     double H, h, ds, dth, x0[3];
+    double ids, idth;    // 1/ds, 1/dth (values only, never decisions)
     int64_t nbox;
     int64_t b0, b1;      // owned box range [b0, b1) (source partition)
     // boxes
@@ -148,7 +150,9 @@ struct ifgf_plan_s {
     std::vector<PendingEv> pending;
     int* dev_bad = nullptr;  // device flag: apply-time invariant violation (EINTERNAL)
     int legacy_upward = 0;   // env IFGF_LEGACY_UPWARD: K7 variant override (A/B testing, tests)
-    int tc_umax = 1 << 30;   // env IFGF_TC_UMAX: cap on staged child cells in the TC K7 (tests the fallback)
+    int tc_umax = 1 << 30;
+    int legacy_cousin = 0;   // env IFGF_LEGACY_COUSIN=1: per-lane global-load K6 (A/B testing)
+    unsigned long long* phase_clk = nullptr;  // env IFGF_PHASE_PROF: TC K7 per-phase clock sums   // env IFGF_TC_UMAX: cap on staged child cells in the TC K7 (tests the fallback)
     int64_t device_bytes = 0;
     std::vector<void*> allocs;  // every cudaMalloc of the plan
 };
@@ -181,8 +185,11 @@ struct Cls {
 // Classification of the relative vector v at a level (DESIGN.md
 // "Classification contract", reading R7).  The
 // discrete decisions use only IEEE-rounded + - * / sqrt without contraction
-// (explicit __d*_rn) against host-libm boundary tables; atan2 only supplies
-// the first guess and the local coordinates.
+// (explicit __d*_rn) against host-libm boundary tables: r, s = h/r,
+// i_s = floor(s/ds), cos(theta) = v_z/r and the phi cross products.  The
+// angles theta = atan2(rho, v_z), phi = atan2(v_y, v_x) (reading R13) come from
+// the lean fm::atan2 and only supply the first guesses (corrected by the exact
+// comparisons) and the local coordinates u = 2 (v - v_a)/dv - 1 (values).
 __device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double vy, double vz) {
     Cls c;
     double r2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
@@ -193,8 +200,8 @@ __device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double 
     // theta: i_theta = #{k in 1..nC-1 : vz/r <= cos(k dtheta)}
     double ct = __ddiv_rn(vz, c.r);
     double rho = __dsqrt_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)));
-    double th = atan2(rho, vz);
-    int it = (int)(th / L.dth);
+    double th = fm::atan2(rho, vz);
+    int it = (int)(th * L.idth);
     it = it < 0 ? 0 : (it > L.nC - 1 ? L.nC - 1 : it);
     while (it > 0 && !(ct <= __ldg(L.cos_tb + it))) --it;
     while (it < L.nC - 1 && ct <= __ldg(L.cos_tb + it + 1)) ++it;
@@ -204,9 +211,9 @@ __device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double 
     double ph = 0.0;
     int ip = 0;
     if (!(vx == 0.0 && vy == 0.0)) {
-        ph = atan2(vy, vx);
+        ph = fm::atan2(vy, vx);
         if (ph < 0.0) ph += 2.0 * kPi;
-        ip = (int)(ph / L.dth);
+        ip = (int)(ph * L.idth);
         ip = ip < 0 ? 0 : (ip > n2 - 1 ? n2 - 1 : ip);
         for (int iter = 0; iter < 2 * n2; ++iter) {
             double cj = __dsub_rn(__dmul_rn(vy, __ldg(L.cphi + ip)), __dmul_rn(vx, __ldg(L.sphi + ip)));
@@ -223,9 +230,10 @@ __device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double 
         }
     }
     c.ip = ip;
-    c.us = 2.0 * (s - c.is * L.ds) / L.ds - 1.0;
-    c.ut = 2.0 * (th - c.it * L.dth) / L.dth - 1.0;
-    c.up = 2.0 * (ph - c.ip * L.dth) / L.dth - 1.0;
+    const double i2s = 2.0 * L.ids, i2t = 2.0 * L.idth;
+    c.us = fma(s - c.is * L.ds, i2s, -1.0);
+    c.ut = fma(th - c.it * L.dth, i2t, -1.0);
+    c.up = fma(ph - c.ip * L.dth, i2t, -1.0);
     return c;
 }
 
@@ -309,6 +317,94 @@ __device__ __forceinline__ double2 contract(const double2* __restrict__ C, const
     double fr = xr[0], fi = xi[0];
 #pragma unroll
     for (int a = 1; a < PS; ++a) {
+        fr = fma(Ts[a], xr[a], fr);
+        fi = fma(Ts[a], xi[a], fi);
+    }
+    return make_double2(fr, fi);
+}
+
+// Tensor contraction from shared memory (same order as contract()).
+template <int PS, int PA>
+__device__ __forceinline__ double2 contract_sm(const double2* C, const double* Ts, const double* Tt, double up) {
+    double wr[PA * PS], wi[PA * PS];
+#pragma unroll
+    for (int i = 0; i < PA * PS; ++i) {
+        double2 v = C[i];
+        wr[i] = v.x;
+        wi[i] = v.y;
+    }
+    double tm1 = 1.0, t = up;
+    const double u2 = 2.0 * up;
+#pragma unroll
+    for (int c = 1; c < PA; ++c) {
+#pragma unroll
+        for (int i = 0; i < PA * PS; ++i) {
+            double2 v = C[c * PA * PS + i];
+            wr[i] = fma(t, v.x, wr[i]);
+            wi[i] = fma(t, v.y, wi[i]);
+        }
+        const double tn = fma(u2, t, -tm1);
+        tm1 = t;
+        t = tn;
+    }
+    double xr[PS], xi[PS];
+#pragma unroll
+    for (int a = 0; a < PS; ++a) {
+        xr[a] = wr[a];
+        xi[a] = wi[a];
+    }
+#pragma unroll
+    for (int b = 1; b < PA; ++b)
+#pragma unroll
+        for (int a = 0; a < PS; ++a) {
+            xr[a] = fma(Tt[b], wr[b * PS + a], xr[a]);
+            xi[a] = fma(Tt[b], wi[b * PS + a], xi[a]);
+        }
+    double fr = xr[0], fi = xi[0];
+#pragma unroll
+    for (int a = 1; a < PS; ++a) {
+        fr = fma(Ts[a], xr[a], fr);
+        fi = fma(Ts[a], xi[a], fi);
+    }
+    return make_double2(fr, fi);
+}
+
+// Same contraction with a small live register set: phi innermost per (a, b)
+// (one complex accumulator), then theta, then s; 3 x 5 x 5 + 15 + 3 complex x
+// real MACs as contract_sm.  Tp is formed from u_phi by the recurrence.
+template <int PS, int PA>
+__device__ __forceinline__ double2 contract_sm_lr(const double2* C, const double* Ts, const double* Tt, double up) {
+    // theta outermost and rolled (T_b by recurrence from Tt[0..1]); per b the
+    // 3 x 5 (s, phi) slab: phi contraction, then accumulate T_b * (.) per s.
+    double Tp[PA];
+    cheb_T<PA>(up, Tp);
+    double xr[PS], xi[PS];
+#pragma unroll
+    for (int a = 0; a < PS; ++a) xr[a] = xi[a] = 0.0;
+    const double ut = PA > 1 ? Tt[1] : 0.0, u2 = 2.0 * ut;
+    double tbm1 = 0.0, tb = 1.0;
+#pragma unroll 1
+    for (int b = 0; b < PA; ++b) {
+        const double2* Cb = C + b * PS;
+#pragma unroll
+        for (int a = 0; a < PS; ++a) {
+            double gr = 0.0, gi = 0.0;
+#pragma unroll
+            for (int c = 0; c < PA; ++c) {
+                const double2 v = Cb[c * PA * PS + a];
+                gr = fma(Tp[c], v.x, gr);
+                gi = fma(Tp[c], v.y, gi);
+            }
+            xr[a] = fma(tb, gr, xr[a]);
+            xi[a] = fma(tb, gi, xi[a]);
+        }
+        const double tn = b == 0 ? ut : fma(u2, tb, -tbm1);
+        tbm1 = tb;
+        tb = tn;
+    }
+    double fr = 0.0, fi = 0.0;
+#pragma unroll
+    for (int a = 0; a < PS; ++a) {
         fr = fma(Ts[a], xr[a], fr);
         fi = fma(Ts[a], xi[a], fi);
     }

@@ -204,6 +204,20 @@ def test_multirank_emulation_one_gpu(ifgf):
         assert oracle.rel_l2(acc, full) < 1e-13, R
 
 
+@pytest.mark.parametrize("legacy", ["0", "1"])
+def test_cousin_kernel_variants(ifgf, legacy, monkeypatch):
+    """K6: the warp-staged kernel (default) and the per-lane global-load kernel
+    (IFGF_LEGACY_COUSIN=1) both match the oracle."""
+    monkeypatch.setenv("IFGF_LEGACY_COUSIN", legacy)
+    n = 20000
+    pts = inputs.rough_sphere(n)
+    a = inputs.densities(n, seed=8)
+    k = 5 * math.pi
+    _, got, _ = run_gpu(ifgf, pts, a, k, 5)
+    ref = oracle.OraclePlan(pts, k, 5, 3, 5).apply(a)
+    assert oracle.rel_l2(got, ref) <= PARITY
+
+
 def test_default_kernel_choice_tc_and_staged(ifgf):
     """At the default settings a lambda/4-leaf sphere uses the FP64 tensor-core
     K7 on its fine levels and the staged DFMA K7 on the coarse ones; both match
