@@ -129,8 +129,9 @@ typedef struct {
     int64_t plan_device_bytes;                         /* device memory held by the plan       */
     double plan_ms;                                    /* wall time of ifgf_plan               */
     int upward_kernel[IFGF_MAX_LEVELS + 1];            /* K7 kernel of the pass d -> d-1:
-                                                          0 staged DFMA, 1 FP64 tensor-core GEMM,
-                                                          -1 no pass (chosen at plan time)        */
+                                                          0 cell-grouped staged DFMA, 1 FP64
+                                                          tensor-core GEMM, 2 per-evaluation
+                                                          DFMA, -1 no pass (chosen at plan time) */
 } ifgf_stats;
 
 ifgf_status ifgf_plan_stats(ifgf_plan_t plan, ifgf_stats* stats);

@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
 //   Interp_{B, gamma(y)} F_B(y) * G(y, c_B)/G(y, c_Q)
 // one thread per (parent segment, node); y - c_B = off + delta, delta = +-H_d/2.
 template <int PS, int PA>
-__global__ void __launch_bounds__(TPB) k_upward(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
+__global__ void __launch_bounds__(TPB, 4) k_upward(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
                                                 double k, int Ps, int Pa, double2* vals_p, int* bad) {
     const int P = Ps * Pa * Pa;
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -382,7 +382,15 @@ __global__ void __launch_bounds__(TPB) k_upward(LevelParams L, LevelParams LP, c
             atomicOr(bad, 1);
             continue;
         }
-        double2 F = interp<PS, PA>(vals_d + slot * P, Ps, Pa, c.us, c.ut, c.up);
+        double2 F;
+        if constexpr (PS > 0) {
+            double Ts[PS], Tt[PA];
+            cheb_T<PS>(c.us, Ts);
+            cheb_T<PA>(c.ut, Tt);
+            F = contract_sm_lr<PS, PA, true>(vals_d + slot * P, Ts, Tt, c.up);
+        } else {
+            F = interp<PS, PA>(vals_d + slot * P, Ps, Pa, c.us, c.ut, c.up);
+        }
         // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
         double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
         double diff = num / (c.r + rQ);
@@ -1398,7 +1406,7 @@ struct Kern {
     static bool upward(dim3 g, cudaStream_t st, const LevelParams& L, const LevelParams& LP, const ifgf_plan_s* p,
                        const double2* vd, double2* vp, int* bad) {
         if constexpr (PS > 0 && PS * PA * PA <= 80) {
-            if (LP.up_tc && LP.nchunk > 0) {
+            if (LP.up_kernel == 1 && LP.nchunk > 0) {
                 using Cfg = TcCfg<PS, PA>;
                 static bool attr = false;
                 if (!attr) {
@@ -1406,15 +1414,13 @@ struct Kern {
                                                    (int)Cfg::smem));
                     attr = true;
                 }
-                k_upward_tc<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(L, LP, vd, p->k, p->cheb_Ms,
-                                                                                       p->cheb_Ma, vp, bad, std::min(Cfg::UM, p->tc_umax),
-                                                                                       p->zseg, p->phase_clk);
+                k_upward_tc<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(
+                    L, LP, vd, p->k, p->cheb_Ms, p->cheb_Ma, vp, bad, std::min(Cfg::UM, p->tc_umax), p->zseg,
+                    p->phase_clk);
                 return true;
             }
-        }
-        if constexpr (PS > 0 && PS * PA * PA <= 80) {
-            // FP64 tensor-core kernel: opt-in (mode 4) until it beats the staged DFMA kernel
-            if (p->legacy_upward == 4 && LP.nchunk > 0) {
+            // FP64 tensor-core kernel on 16-chunks (A/B variant 4)
+            if (LP.up_kernel == 0 && p->legacy_upward == 4 && LP.nchunk > 0) {
                 using Cfg = MmaCfg<PS, PA>;
                 static bool attr = false;
                 if (!attr) {
@@ -1428,7 +1434,13 @@ struct Kern {
             }
         }
         if constexpr (PS > 0 && PS * PA * PA <= 128) {
-            if (LP.nchunk > 0 && (p->legacy_upward == 0 || p->legacy_upward == 3)) {
+            if (LP.up_kernel == 0 && LP.nchunk > 0 && p->legacy_upward == 2) {
+                constexpr int P = PS * PA * PA;
+                const int threads = ((P + 31) / 32) * 32;
+                k_upward_g<PS, PA><<<(unsigned)LP.nchunk, threads, 0, st>>>(L, LP, vd, p->k, vp, bad);
+                return false;
+            }
+            if (LP.up_kernel == 0 && LP.nchunk > 0) {
                 using Cfg = StagedCfg<PS, PA>;
                 static bool attr = false;
                 if (!attr) {
@@ -1439,12 +1451,6 @@ struct Kern {
                 k_upward_s<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(L, LP, vd, p->k, p->cheb_Ms,
                                                                                       p->cheb_Ma, vp, bad);
                 return true;
-            }
-            if (LP.nchunk > 0 && p->legacy_upward == 2) {
-                constexpr int P = PS * PA * PA;
-                const int threads = ((P + 31) / 32) * 32;
-                k_upward_g<PS, PA><<<(unsigned)LP.nchunk, threads, 0, st>>>(L, LP, vd, p->k, vp, bad);
-                return false;
             }
         }
         k_upward<PS, PA><<<g, TPB, 0, st>>>(L, LP, vd, p->k, p->Ps, p->Pa, vp, bad);

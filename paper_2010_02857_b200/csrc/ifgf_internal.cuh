@@ -86,10 +86,11 @@ struct LevelParams {  // passed by value to kernels
     const int* cell_seg;
     const int* chunk_start;
     int64_t nchunk;
-    // K7 kernel of the level when it is the PARENT level: 0 = staged DFMA kernel
-    // (chunks of <= kChunk segments), 1 = FP64 tensor-core kernel (chunks of
-    // <= kChunkTC segments); chosen at plan time from the segments per cell.
-    int up_tc;
+    // K7 kernel of the pass into this level (as PARENT level), chosen at plan time
+    // from the segments per cell: 0 = cell-grouped staged DFMA (chunks of
+    // <= kChunk), 1 = FP64 tensor-core GEMM (chunks of <= kChunkTC), 2 =
+    // per-evaluation geometry (no chunks, separate K5 fit)
+    int up_kernel;
 };
 
 constexpr int kChunk = 16;
@@ -372,7 +373,7 @@ __device__ __forceinline__ double2 contract_sm(const double2* C, const double* T
 // Same contraction with a small live register set: phi innermost per (a, b)
 // (one complex accumulator), then theta, then s; 3 x 5 x 5 + 15 + 3 complex x
 // real MACs as contract_sm.  Tp is formed from u_phi by the recurrence.
-template <int PS, int PA>
+template <int PS, int PA, bool GLOBAL = false>
 __device__ __forceinline__ double2 contract_sm_lr(const double2* C, const double* Ts, const double* Tt, double up) {
     // theta outermost and rolled (T_b by recurrence from Tt[0..1]); per b the
     // 3 x 5 (s, phi) slab: phi contraction, then accumulate T_b * (.) per s.
@@ -391,7 +392,7 @@ __device__ __forceinline__ double2 contract_sm_lr(const double2* C, const double
             double gr = 0.0, gi = 0.0;
 #pragma unroll
             for (int c = 0; c < PA; ++c) {
-                const double2 v = Cb[c * PA * PS + a];
+                const double2 v = GLOBAL ? __ldg(Cb + c * PA * PS + a) : Cb[c * PA * PS + a];
                 gr = fma(Tp[c], v.x, gr);
                 gi = fma(Tp[c], v.y, gi);
             }

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -867,11 +868,19 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         inclusive_scan(S, flag, incl, ns, st);
         const int64_t nrun = d2h_one(incl + ns - 1, st);
         const double per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
-        int tc = per_run >= 24.0 ? 1 : 0;
-        if (p->legacy_upward >= 1 && p->legacy_upward <= 4) tc = 0;  // legacy A/B variants: 16-chunks
-        if (p->legacy_upward == 5) tc = 1;                           // force the tensor-core kernel
-        if (P > 80) tc = 0;  // TC kernel shared memory is sized for P <= 80 (P_s, P_ang) = (3, 5)
-        L.p.up_tc = tc;
+        // K7 kernel by mean segments per cell run (measured on B200):
+        // many -> FP64 tensor-core GEMM; some -> cell-grouped staged DFMA; ~1-2 ->
+        // per-evaluation geometry (nothing to share, least overhead)
+        int kern = per_run >= 24.0 ? 1 : (per_run >= 6.0 ? 0 : 2);
+        if (p->legacy_upward == 1) kern = 2;
+        if (p->legacy_upward >= 2 && p->legacy_upward <= 4) kern = 0;  // 16-chunk variants
+        if (p->legacy_upward == 5) kern = 1;                           // force the tensor-core kernel
+        if (P > 80 && kern == 1) kern = 0;  // TC kernel shared memory is sized for P <= 80 ((P_s, P_ang) = (3, 5))
+        const int tc = kern == 1;
+        L.p.up_kernel = kern;
+        if (std::getenv("IFGF_PLAN_VERBOSE"))
+            fprintf(stderr, "[ifgf] level %d: %lld segments, %lld cell runs, %.2f per run, K7 kernel %d\n", d,
+                    (long long)ns, (long long)nrun, per_run, kern);
         k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, tc ? kChunkTC : kChunk, flag);
         inclusive_scan(S, flag, incl, ns, st);
         int64_t nch = d2h_one(incl + ns - 1, st);
@@ -925,7 +934,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             s.cousin_evals[d] = d >= 3 ? (int64_t)h[4 * d] : 0;
             s.upward_evals[d] = d >= 4 ? (int64_t)h[4 * d + 1] : 0;
             s.segment_bytes[d] = 16LL * P * p->lev[d].p.nseg;
-            s.upward_kernel[d] = (d >= 4 && p->lev[d - 1].p.nseg > 0) ? p->lev[d - 1].p.up_tc : -1;
+            s.upward_kernel[d] = (d >= 4 && p->lev[d - 1].p.nseg > 0) ? p->lev[d - 1].p.up_kernel : -1;
         }
     }
 

@@ -227,7 +227,7 @@ def test_default_kernel_choice_tc_and_staged(ifgf):
     a = inputs.densities(n, seed=5)
     _, got, st = run_gpu(ifgf, pts, a, k, D)
     kern = st["upward_kernel"]
-    assert kern[D] == 1 and kern[4] == 0, kern
+    assert kern[D] == 1 and kern[4] in (0, 2), kern
     ref = oracle.OraclePlan(pts, k, D, 3, 5).apply(a)
     assert oracle.rel_l2(got, ref) <= PARITY
 
@@ -256,8 +256,8 @@ def test_upward_kernel_variants(ifgf, mode, umax, monkeypatch):
     tensor-core GEMM kernel on 64-chunks at every level) matches the oracle.
     IFGF_TC_UMAX caps the child cells the TC kernel stages per octant, so that its
     per-node fallback (taken near the poles) is exercised too.  The default (0)
-    picks the TC kernel where many segments share a cell, the staged kernel
-    elsewhere."""
+    picks the TC kernel where many segments share a cell, the staged kernel where
+    some do, the per-evaluation kernel where ~1-2 do."""
     monkeypatch.setenv("IFGF_LEGACY_UPWARD", mode)
     if umax is not None:
         monkeypatch.setenv("IFGF_TC_UMAX", umax)
