@@ -44,9 +44,12 @@ CPU_SAMPLE_DESC = ("oracle apply (serial C++, 1 thread) on the cfg4 workload fam
 
 
 def algorithmic_flops_per_upward_eval(Ps: int, Pa: int) -> float:
-    """separable tensor contraction (complex x real MAC = 4
-    flops) 4 (P + P_s P_ang + P_s) + recentering complex MAC (8)."""
-    return 4.0 * (Ps * Pa * Pa + Ps * Pa + Ps) + 8.0
+    """DESIGN.md §7 / SURVEY.md §8(d) ("~310 with a precomputed tensor basis"):
+    every one of the P coefficients enters one complex x real MAC (4 flops), plus
+    the recentering complex MAC (8 flops).  Geometry (classification, atan2,
+    sincos, divisions) and padding are not counted, so the fraction understates
+    the FP64 pipe's real load."""
+    return 4.0 * (Ps * Pa * Pa) + 8.0
 
 
 class ClockSampler:
@@ -269,7 +272,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "rel_err_vs_direct": rel_err,
             "plan_ms": plan_s * 1e3,
             "kernel_ms_per_step": kernel_ms,
-            "roofline": {"kernel": "K7 upward (k_upward)", "bound": "alu", "achieved": achieved / 1e12,
+            "roofline": {"kernel": "K7 upward (k_upward_tc / k_upward_s / k_upward_pe, all levels)", "bound": "alu", "achieved": achieved / 1e12,
                          "peak": dfma_flops / 1e12, "unit": "TFLOP/s", "frac": achieved / dfma_flops,
                          "traffic": traffic,
                          "peak_source": "FP64 DFMA microbenchmark (ifgf_bench_dfma) measured in this run; "

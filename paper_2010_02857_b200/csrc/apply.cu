@@ -355,6 +355,106 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
     }
 }
 
+// K7, per-evaluation geometry, warp-staged and pipelined (coarse levels, where
+// ~1-2 parent segments share a cone cell).  Lane = (parent segment, node) of the
+// level, 32 consecutive ones per warp; the warp walks the child octants o = 0..7:
+// each lane classifies its node relative to child B_o of its segment, the warp
+// elects the distinct child segments (<= SMAX), copies them into its
+// shared-memory slots with cp.async and every lane contracts from its slot.
+// Octant o+1 is classified and its copies issued before octant o is
+// contracted.  Output: node values (the K5 fit runs after).
+template <int PS, int PA>
+__global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams LP,
+                                                      const double2* __restrict__ vals_d, double k, double2* vals_p,
+                                                      int* bad) {
+    constexpr int P = PS * PA * PA;
+    constexpr int SMAX = P <= 80 ? 4 : 2;
+    constexpr int SP = P + 2;
+    __shared__ __align__(16) double2 sbuf[TPB / 32][2][SMAX][SP];
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if ((t & ~(int64_t)31) >= LP.nseg * P) return;  // warp-uniform
+    const bool active = t < LP.nseg * P;
+    const int64_t sp = active ? t / P : 0;
+    const int n = active ? (int)(t - sp * P) : 0;
+    double off[3] = {0.0, 0.0, 0.0};
+    int Q = -1;
+    if (active) {
+        Q = LP.seg_box[sp];
+        node_off(LP, PS, PA, LP.seg_cell[sp], n, off);
+    }
+    const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
+    const double hh = 0.5 * L.H;
+    struct Ev {
+        int64_t slot;
+        int bi;
+        double rr, ri, us, ut, up;
+    };
+    auto prep = [&](int o, Ev& v, int buf) {
+        v.slot = -1;
+        v.bi = -1;
+        int B = active ? LP.child_oct[8 * Q + o] : -1;
+        if (B < L.b0 || B >= L.b1) B = -1;
+        if (B >= 0) {
+            const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
+            const Cls c = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+            v.slot = seg_slot(L, B, cell_of(L, c));
+            if (v.slot < 0) atomicOr(bad, 1);
+            // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
+            const double num =
+                fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
+            const double diff = num / (c.r + rQ);
+            const double ratio = rQ / c.r;
+            double sn, cs;
+            fm::sincos(k * diff, &sn, &cs);
+            v.rr = ratio * cs;
+            v.ri = ratio * sn;
+            v.us = c.us;
+            v.ut = c.ut;
+            v.up = c.up;
+        }
+        unsigned pend = __ballot_sync(~0u, v.slot >= 0);
+        int nd = 0;
+        while (pend && nd < SMAX) {
+            const int leader = __ffs(pend) - 1;
+            const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
+            const double2* src = vals_d + s0 * P;
+            double2* dst = &sbuf[w][buf][nd][0];
+            for (int i = lane; i < P; i += 32) cp_async16(dst + i, src + i);
+            const bool mine = v.slot == s0;
+            if (mine) v.bi = nd;
+            pend &= ~__ballot_sync(~0u, mine);
+            ++nd;
+        }
+        cp_async_commit();
+    };
+    double ar = 0.0, ai = 0.0;
+    Ev cur, nxt;
+    prep(0, cur, 0);
+#pragma unroll 1
+    for (int o = 0; o < 8; ++o) {
+        if (o + 1 < 8) {
+            prep(o + 1, nxt, (o + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        if (cur.slot >= 0) {
+            double Ts[PS], Tt[PA];
+            cheb_T<PS>(cur.us, Ts);
+            cheb_T<PA>(cur.ut, Tt);
+            const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA>(&sbuf[w][o & 1][cur.bi][0], Ts, Tt, cur.up)
+                                          : contract_sm_lr<PS, PA, true>(vals_d + cur.slot * P, Ts, Tt, cur.up);
+            ar = fma(cur.rr, F.x, fma(-cur.ri, F.y, ar));
+            ai = fma(cur.rr, F.y, fma(cur.ri, F.x, ai));
+        }
+        __syncwarp();  // slot buffer (o & 1) is refilled by prep(o + 2)
+        cur = nxt;
+    }
+    if (active) vals_p[t] = make_double2(ar, ai);
+}
+
 // K7: V_Q[gamma', y] = sum over owned children B of Q of
 //   Interp_{B, gamma(y)} F_B(y) * G(y, c_B)/G(y, c_Q)
 // one thread per (parent segment, node); y - c_B = off + delta, delta = +-H_d/2.
@@ -1451,6 +1551,12 @@ struct Kern {
                 k_upward_s<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(L, LP, vd, p->k, p->cheb_Ms,
                                                                                       p->cheb_Ma, vp, bad);
                 return true;
+            }
+        }
+        if constexpr (PS > 0) {
+            if (p->legacy_upward != 1) {
+                k_upward_pe<PS, PA><<<g, TPB, 0, st>>>(L, LP, vd, p->k, vp, bad);
+                return false;
             }
         }
         k_upward<PS, PA><<<g, TPB, 0, st>>>(L, LP, vd, p->k, p->Ps, p->Pa, vp, bad);

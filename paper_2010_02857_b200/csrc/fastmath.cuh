@@ -37,7 +37,74 @@ constexpr double kPiHi = 3.141592653589793, kPiLo = 1.2246467991473532e-16;
 constexpr double k2OverPi = 0.6366197723675814;
 constexpr double kPio2_1 = 1.5707963267948966, kPio2_2 = 6.123233995736766e-17, kPio2_3 = -1.4973849048591698e-33;
 
-// Polynomial coefficients: see the header comment.
+// Polynomial coefficients (highest degree first), see the header comment.  On the
+// device they live in constant memory so each DFMA reads its coefficient straight
+// from the constant bank (no per-use 64-bit immediate materialisation).
+#ifdef __CUDACC__
+static __constant__ double kAtanQ_d[11] = {
+    -0.019176887119062258989,
+    0.039231658295587191303,
+    -0.050854497379402598613,
+    0.058581489128022098816,
+    -0.066645114473819480001,
+    0.076921831908260865637,
+    -0.090909045781239018905,
+    0.11111111015256361727,
+    -0.14285714284666542922,
+    0.19999999999995520678,
+    -0.3333333333333333016};
+#endif
+static constexpr double kAtanQ_h[11] = {
+    -0.019176887119062258989,
+    0.039231658295587191303,
+    -0.050854497379402598613,
+    0.058581489128022098816,
+    -0.066645114473819480001,
+    0.076921831908260865637,
+    -0.090909045781239018905,
+    0.11111111015256361727,
+    -0.14285714284666542922,
+    0.19999999999995520678,
+    -0.3333333333333333016};
+#ifdef __CUDACC__
+static __constant__ double kSinS_d[7] = {
+    -7.5866970028175042058e-13,
+    1.6058531617037151954e-10,
+    -2.5052106232435281095e-8,
+    2.7557319219339131119e-6,
+    -0.00019841269841265064901,
+    0.0083333333333333314921,
+    -0.16666666666666666666};
+#endif
+static constexpr double kSinS_h[7] = {
+    -7.5866970028175042058e-13,
+    1.6058531617037151954e-10,
+    -2.5052106232435281095e-8,
+    2.7557319219339131119e-6,
+    -0.00019841269841265064901,
+    0.0083333333333333314921,
+    -0.16666666666666666666};
+#ifdef __CUDACC__
+static __constant__ double kCosC_d[6] = {
+    -1.1382632258093614476e-11,
+    2.0876146266079308857e-9,
+    -2.7557317271718642711e-7,
+    0.000024801587298765666432,
+    -0.0013888888888887397222,
+    0.041666666666666665389};
+#endif
+static constexpr double kCosC_h[6] = {
+    -1.1382632258093614476e-11,
+    2.0876146266079308857e-9,
+    -2.7557317271718642711e-7,
+    0.000024801587298765666432,
+    -0.0013888888888887397222,
+    0.041666666666666665389};
+#ifdef __CUDA_ARCH__
+#define IFGF_FMC(name, i) name##_d[i]
+#else
+#define IFGF_FMC(name, i) name##_h[i]
+#endif
 
 // atan2(y, x) in (-pi, pi]; (x, y) != (0, 0).
 IFGF_HD double atan2(double y, double x) {
@@ -46,21 +113,24 @@ IFGF_HD double atan2(double y, double x) {
     const bool big = mn > kTanPi8 * mx;  // reduce via atan(t) = pi/4 + atan((t-1)/(t+1))
     const double t = (big ? mn - mx : mn) / (big ? mn + mx : mx);
     const double s = t * t;
-    double q = -0.019176887119062258989;
-    q = std::fma(q, s, 0.039231658295587191303);
-    q = std::fma(q, s, -0.050854497379402598613);
-    q = std::fma(q, s, 0.058581489128022098816);
-    q = std::fma(q, s, -0.066645114473819480001);
-    q = std::fma(q, s, 0.076921831908260865637);
-    q = std::fma(q, s, -0.090909045781239018905);
-    q = std::fma(q, s, 0.11111111015256361727);
-    q = std::fma(q, s, -0.14285714284666542922);
-    q = std::fma(q, s, 0.19999999999995520678);
-    q = std::fma(q, s, -0.3333333333333333016);
+    double q = IFGF_FMC(kAtanQ, 0);
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 1));
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 2));
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 3));
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 4));
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 5));
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 6));
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 7));
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 8));
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 9));
+    q = std::fma(q, s, IFGF_FMC(kAtanQ, 10));
     double r = std::fma(t * s, q, t);  // atan(mn / mx) (- pi/4 if big)
-    if (big) r = kPi4 + (r + kPi4Lo);
-    if (ay > ax) r = kPi2 - (r - kPi2Lo);
-    if (x < 0.0) r = kPiHi - (r - kPiLo);
+    const double r1 = kPi4 + (r + kPi4Lo);
+    r = big ? r1 : r;
+    const double r2 = kPi2 - (r - kPi2Lo);
+    r = ay > ax ? r2 : r;
+    const double r3 = kPiHi - (r - kPiLo);
+    r = x < 0.0 ? r3 : r;
     return std::copysign(r, y);
 }
 
@@ -80,19 +150,19 @@ IFGF_HD void sincos(double x, double* sp, double* cp) {
     r = std::fma(-q, kPio2_2, r);
     r = std::fma(-q, kPio2_3, r);
     const double s = r * r;
-    double ps = -7.5866970028175042058e-13;
-    ps = std::fma(ps, s, 1.6058531617037151954e-10);
-    ps = std::fma(ps, s, -2.5052106232435281095e-8);
-    ps = std::fma(ps, s, 2.7557319219339131119e-6);
-    ps = std::fma(ps, s, -0.00019841269841265064901);
-    ps = std::fma(ps, s, 0.0083333333333333314921);
-    ps = std::fma(ps, s, -0.16666666666666666666);
-    double pc = -1.1382632258093614476e-11;
-    pc = std::fma(pc, s, 2.0876146266079308857e-9);
-    pc = std::fma(pc, s, -2.7557317271718642711e-7);
-    pc = std::fma(pc, s, 0.000024801587298765666432);
-    pc = std::fma(pc, s, -0.0013888888888887397222);
-    pc = std::fma(pc, s, 0.041666666666666665389);
+    double ps = IFGF_FMC(kSinS, 0);
+    ps = std::fma(ps, s, IFGF_FMC(kSinS, 1));
+    ps = std::fma(ps, s, IFGF_FMC(kSinS, 2));
+    ps = std::fma(ps, s, IFGF_FMC(kSinS, 3));
+    ps = std::fma(ps, s, IFGF_FMC(kSinS, 4));
+    ps = std::fma(ps, s, IFGF_FMC(kSinS, 5));
+    ps = std::fma(ps, s, IFGF_FMC(kSinS, 6));
+    double pc = IFGF_FMC(kCosC, 0);
+    pc = std::fma(pc, s, IFGF_FMC(kCosC, 1));
+    pc = std::fma(pc, s, IFGF_FMC(kCosC, 2));
+    pc = std::fma(pc, s, IFGF_FMC(kCosC, 3));
+    pc = std::fma(pc, s, IFGF_FMC(kCosC, 4));
+    pc = std::fma(pc, s, IFGF_FMC(kCosC, 5));
     const double sn = std::fma(r * s, ps, r);
     const double cs = std::fma(s * s, pc, std::fma(-0.5, s, 1.0));
     const int iq = (int)(long long)q & 3;

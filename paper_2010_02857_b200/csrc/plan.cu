@@ -834,53 +834,63 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         k_iota<<<nblocks(ns), TPB, 0, st>>>(ns, vals_in);
         int bits = 1;
         while (bits < 31 && ((int64_t)1 << bits) < L.p.ncell) ++bits;
-        // L2 tiles: consecutive parent boxes whose children's coefficients total
-        // ~32 MB; segments are grouped by cell only inside a tile (locality).
+        // Tiles: consecutive parent boxes whose children's coefficients total
+        // tile_bytes; segments are grouped by cell only inside a tile.  Large tiles
+        // give long cell runs (geometry reuse); where runs are very long (fine
+        // levels) the tile shrinks so that a tile's child data stays L2-resident
+        // while its cells' chunks run (target ~256 segments per run).
         const double child_bytes_per_box =
             (double)p->lev[d + 1].p.nseg * P * 16.0 / (double)std::max<int64_t>(1, L.p.b1 - L.p.b0);
-        double tile_bytes = 4096.0e6;  // child bytes per tile (env IFGF_TILE_MB)
-        if (const char* e = std::getenv("IFGF_TILE_MB")) tile_bytes = std::atof(e) * 1.0e6;
-        int64_t tile = (int64_t)std::max(1.0, tile_bytes / std::max(1.0, child_bytes_per_box));
-        int tbits = 1;
-        while (tbits < 32 && ((int64_t)1 << tbits) <= L.p.nbox / tile + 1) ++tbits;
-        k_tile_keys<<<nblocks(ns), TPB, 0, st>>>(L.seg_box, L.seg_cell, ns, tile, bits, keys_in);
-        size_t bytes = 0;
-        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, keys_out, vals_in, L.cell_seg, (int)ns, 0,
-                                                  bits + tbits, st));
-        void* tmp = S.get<char>((int64_t)bytes);
-        IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_in, keys_out, vals_in, L.cell_seg, (int)ns, 0,
-                                                  bits + tbits, st));
-        S.release(tmp);
-        S.release(keys_in);
+        double tile_bytes = 4096.0e6;  // child bytes per tile (env IFGF_TILE_MB: fixed)
+        const char* tile_env = std::getenv("IFGF_TILE_MB");
+        if (tile_env) tile_bytes = std::atof(tile_env) * 1.0e6;
         int* rs = S.get<int>(ns);
         int* rsm = S.get<int>(ns);
-        k_run_start<<<nblocks(ns), TPB, 0, st>>>(keys_out, ns, rs);
-        bytes = 0;
-        IFGF_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, rs, rsm, MaxOp(), (int)ns, st));
-        tmp = S.get<char>((int64_t)bytes);
-        IFGF_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, rs, rsm, MaxOp(), (int)ns, st));
-        S.release(tmp);
-        int* flag = rs;  // reuse
         int* incl = S.get<int>(ns);
-        // runs of equal (tile, cell): their mean length picks the K7 kernel of this
-        // parent level (tensor-core GEMM when many segments share a cell)
-        k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, 0x7fffffff, flag);
-        inclusive_scan(S, flag, incl, ns, st);
-        const int64_t nrun = d2h_one(incl + ns - 1, st);
-        const double per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
+        int* flag = rs;  // reused after the run-start max-scan
+        auto group = [&](double tb) -> int64_t {  // sort by (tile, cell, segment); number of runs
+            const int64_t tile = (int64_t)std::max(1.0, tb / std::max(1.0, child_bytes_per_box));
+            int tbits = 1;
+            while (tbits < 32 && ((int64_t)1 << tbits) <= L.p.nbox / tile + 1) ++tbits;
+            k_tile_keys<<<nblocks(ns), TPB, 0, st>>>(L.seg_box, L.seg_cell, ns, tile, bits, keys_in);
+            size_t bytes = 0;
+            IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, keys_out, vals_in, L.cell_seg, (int)ns,
+                                                      0, bits + tbits, st));
+            void* tmp = S.get<char>((int64_t)bytes);
+            IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_in, keys_out, vals_in, L.cell_seg, (int)ns, 0,
+                                                      bits + tbits, st));
+            S.release(tmp);
+            k_run_start<<<nblocks(ns), TPB, 0, st>>>(keys_out, ns, rs);
+            bytes = 0;
+            IFGF_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, rs, rsm, MaxOp(), (int)ns, st));
+            tmp = S.get<char>((int64_t)bytes);
+            IFGF_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, rs, rsm, MaxOp(), (int)ns, st));
+            S.release(tmp);
+            k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, 0x7fffffff, flag);
+            inclusive_scan(S, flag, incl, ns, st);
+            return d2h_one(incl + ns - 1, st);
+        };
+        int64_t nrun = group(tile_bytes);
+        double per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
+        if (!tile_env && per_run > 1024.0) {
+            tile_bytes = std::max(32.0e6, tile_bytes * 256.0 / per_run);
+            nrun = group(tile_bytes);
+            per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
+        }
+        S.release(keys_in);
         // K7 kernel by mean segments per cell run (measured on B200):
         // many -> FP64 tensor-core GEMM; some -> cell-grouped staged DFMA; ~1-2 ->
         // per-evaluation geometry (nothing to share, least overhead)
         int kern = per_run >= 24.0 ? 1 : (per_run >= 6.0 ? 0 : 2);
-        if (p->legacy_upward == 1) kern = 2;
+        if (p->legacy_upward == 1 || p->legacy_upward == 7) kern = 2;  // per-evaluation (1: per-lane loads)
         if (p->legacy_upward >= 2 && p->legacy_upward <= 4) kern = 0;  // 16-chunk variants
         if (p->legacy_upward == 5) kern = 1;                           // force the tensor-core kernel
         if (P > 80 && kern == 1) kern = 0;  // TC kernel shared memory is sized for P <= 80 ((P_s, P_ang) = (3, 5))
         const int tc = kern == 1;
         L.p.up_kernel = kern;
         if (std::getenv("IFGF_PLAN_VERBOSE"))
-            fprintf(stderr, "[ifgf] level %d: %lld segments, %lld cell runs, %.2f per run, K7 kernel %d\n", d,
-                    (long long)ns, (long long)nrun, per_run, kern);
+            fprintf(stderr, "[ifgf] level %d: %lld segments, %lld cell runs, %.2f per run, tile %.0f MB, K7 kernel %d\n",
+                    d, (long long)ns, (long long)nrun, per_run, tile_bytes / 1e6, kern);
         k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, tc ? kChunkTC : kChunk, flag);
         inclusive_scan(S, flag, incl, ns, st);
         int64_t nch = d2h_one(incl + ns - 1, st);

@@ -249,11 +249,12 @@ def test_cfg2_parity(ifgf):
 
 
 @pytest.mark.parametrize("mode,umax", [("1", None), ("2", None), ("3", None), ("4", None), ("5", None),
-                                       ("5", "1"), ("5", "0")])
+                                       ("5", "1"), ("5", "0"), ("7", None)])
 def test_upward_kernel_variants(ifgf, mode, umax, monkeypatch):
     """Every K7 variant (1 per-evaluation geometry, 2 cell-grouped, 3 cell-grouped
     + shared-memory staged, 4 FP64 tensor-core DMMA on 16-chunks, 5 the FP64
-    tensor-core GEMM kernel on 64-chunks at every level) matches the oracle.
+    tensor-core GEMM kernel on 64-chunks at every level, 7 the warp-staged
+    per-evaluation kernel at every level) matches the oracle.
     IFGF_TC_UMAX caps the child cells the TC kernel stages per octant, so that its
     per-node fallback (taken near the poles) is exercised too.  The default (0)
     picks the TC kernel where many segments share a cell, the staged kernel where
