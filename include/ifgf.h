@@ -131,7 +131,8 @@ typedef struct {
     int upward_kernel[IFGF_MAX_LEVELS + 1];            /* K7 kernel of the pass d -> d-1:
                                                           0 cell-grouped staged DFMA, 1 FP64
                                                           tensor-core GEMM, 2 per-evaluation
-                                                          DFMA, -1 no pass (chosen at plan time) */
+                                                          DFMA, 3 register-basis FP64 tensor-core
+                                                          GEMM, -1 no pass (chosen at plan time) */
 } ifgf_stats;
 
 ifgf_status ifgf_plan_stats(ifgf_plan_t plan, ifgf_stats* stats);

@@ -44,36 +44,62 @@ __global__ void k_unpermute(const double2* __restrict__ in, const int* __restric
 
 // K3: out[l] = sum over owned neighbour boxes B of the leaf T containing l,
 // sum_{m in B, m != l} a_m e^{ik r}/(4 pi r)  (raw kernel, reading R11).
-// One warp per (leaf, 32 targets); sources are read as warp-uniform broadcasts.
+// One warp per (leaf, 32 targets).  The neighbours' sources are staged per warp
+// in shared memory in chunks of 32 (one coalesced load per lane), then every
+// lane sweeps the chunk (broadcast reads); 1/r from one rsqrt, phase by fm::sincos.
 __global__ void __launch_bounds__(TPB) k_near(LevelParams L, const double* __restrict__ px,
                                               const double* __restrict__ py, const double* __restrict__ pz,
                                               const double2* __restrict__ a, double k, double2* out) {
-    int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (item >= L.nwitems) return;
-    int2 it = L.witems[item];
-    int T = it.x, l = it.y + lane;
-    if (l >= L.box_start[T + 1]) return;
-    const double x = px[l], y = py[l], z = pz[l];
+    __shared__ double sx[TPB / 32][32], sy[TPB / 32][32], sz[TPB / 32][32];
+    __shared__ double2 sa[TPB / 32][32];
+    const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (item >= L.nwitems) return;  // warp-uniform
+    const int2 it = L.witems[item];
+    const int T = it.x, l = it.y + lane;
+    const bool active = l < L.box_start[T + 1];
+    double x = 0.0, y = 0.0, z = 0.0;
+    if (active) {
+        x = px[l];
+        y = py[l];
+        z = pz[l];
+    }
     double ar = 0.0, ai = 0.0;
-    for (int e = L.nbr_off[T]; e < L.nbr_off[T + 1]; ++e) {
-        int B = L.nbr_idx[e];
+    const int e1 = L.nbr_off[T + 1];
+    for (int e = L.nbr_off[T]; e < e1; ++e) {
+        const int B = L.nbr_idx[e];
         if (B < L.b0 || B >= L.b1) continue;
-        int m1 = L.box_start[B + 1];
-        for (int m = L.box_start[B]; m < m1; ++m) {
-            if (m == l) continue;
-            double dx = x - px[m], dy = y - py[m], dz = z - pz[m];
-            double r = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
-            double s, c;
-            sincos(k * r, &s, &c);
-            double w = kInv4Pi / r;
-            double2 am = a[m];
-            double gr = c * w, gi = s * w;
-            ar = fma(am.x, gr, fma(-am.y, gi, ar));
-            ai = fma(am.x, gi, fma(am.y, gr, ai));
+        const int m0 = L.box_start[B], m1 = L.box_start[B + 1];
+        for (int c0 = m0; c0 < m1; c0 += 32) {
+            const int cn = min(32, m1 - c0);
+            __syncwarp();
+            if (lane < cn) {
+                sx[w][lane] = px[c0 + lane];
+                sy[w][lane] = py[c0 + lane];
+                sz[w][lane] = pz[c0 + lane];
+                sa[w][lane] = a[c0 + lane];
+            }
+            __syncwarp();
+            if (active) {
+#pragma unroll 2
+                for (int t = 0; t < cn; ++t) {
+                    if (c0 + t == l) continue;
+                    const double dx = x - sx[w][t], dy = y - sy[w][t], dz = z - sz[w][t];
+                    const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+                    const double ri = rsqrt(r2);
+                    const double r = r2 * ri;
+                    double sn, cs;
+                    fm::sincos(k * r, &sn, &cs);
+                    const double wr = kInv4Pi * ri;
+                    const double2 am = sa[w][t];
+                    const double gr = cs * wr, gi = sn * wr;
+                    ar = fma(am.x, gr, fma(-am.y, gi, ar));
+                    ai = fma(am.x, gi, fma(am.y, gr, ai));
+                }
+            }
         }
     }
-    out[l] = make_double2(ar, ai);
+    if (active) out[l] = make_double2(ar, ai);
 }
 
 __device__ __forceinline__ void node_off(const LevelParams& LP, int Ps, int Pa, int cell, int n, double off[3]) {
@@ -136,13 +162,15 @@ __global__ void __launch_bounds__(TPB) k_s2c(LevelParams L, const double* __rest
                 for (int t = 0; t < cn; ++t) {
                     double wx = sw[t][0], wy = sw[t][1], wz = sw[t][2];
                     double dx = off[0] - wx, dy = off[1] - wy, dz = off[2] - wz;
-                    double rd = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
+                    const double d2 = fma(dx, dx, fma(dy, dy, dz * dz));
+                    const double rdi = rsqrt(d2);
+                    const double rd = d2 * rdi;
                     // |y - x_m| - |y - c| = (w.w - 2 off.w) / (|off - w| + |off|)   (reading R17)
                     double num = fma(wx, wx, fma(wy, wy, wz * wz)) - 2.0 * fma(off[0], wx, fma(off[1], wy, off[2] * wz));
-                    double diff = num / (rd + ro);
-                    double ratio = ro / rd;
+                    double diff = num * __drcp_rn(rd + ro);
+                    double ratio = ro * rdi;
                     double sn, cs;
-                    sincos(k * diff, &sn, &cs);
+                    fm::sincos(k * diff, &sn, &cs);
                     double gr = ratio * cs, gi = ratio * sn;
                     double2 am = sa[t];
                     vr = fma(am.x, gr, fma(-am.y, gi, vr));
@@ -1084,7 +1112,8 @@ struct TcCfg {
     static constexpr int KP = ((4 * KS) % 16 == 4 || (4 * KS) % 16 == 12) ? 4 * KS : 4 * KS + 4;
     static constexpr int J = kChunkTC;
     static constexpr int UM = 8;              // distinct child cells per octant with staged slots
-    static constexpr int NT = 256;
+    static constexpr int NT = 384;                 // 12 warps (measured best: 8 with prefetch, 16 spill)
+    static constexpr bool PREFETCH = NT <= 256;  // register double buffer of B fragments
     static constexpr int NWARP = NT / 32;
     static constexpr int R = (NW + 31) / 32;
     static constexpr int FG = 16;             // fit group (segments)
@@ -1110,7 +1139,7 @@ struct TcCfg {
 };
 
 template <int PS, int PA>
-__global__ void __launch_bounds__(256, 1) k_upward_tc(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
+__global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
                                                       double k, const double* __restrict__ Ms,
                                                       const double* __restrict__ Ma, double2* vals_p, int* bad,
                                                       int umax, const double2* __restrict__ zseg,
@@ -1281,6 +1310,7 @@ __global__ void __launch_bounds__(256, 1) k_upward_tc(LevelParams L, LevelParams
 
     // ---- phase 4: per octant, W_o then DMMA tasks
     const int gid = lane >> 2, tig = lane & 3;
+    long long t_task0 = 0;
     for (int o = 0; o < 8; ++o) {
         const int no = sNo[o];
         if (no == 0) continue;
@@ -1317,6 +1347,7 @@ __global__ void __launch_bounds__(256, 1) k_upward_tc(LevelParams L, LevelParams
             }
             __syncthreads();
             mark(4);
+            t_task0 = clock64();
             // Tasks (segment tile st, child cell ui, node tile) enumerated st-major;
             // warp w takes the contiguous range [w T / NWARP, (w+1) T / NWARP), so
             // consecutive tasks mostly share (st, ui) and its B fragments stay in
@@ -1350,7 +1381,7 @@ __global__ void __launch_bounds__(256, 1) k_upward_tc(LevelParams L, LevelParams
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) bb[ks] = __ldg(cp + 4 * ks + tig);
             };
-            double2 bc[KS], bn[KS];
+            double2 bc[KS], bn[C::PREFETCH ? KS : 1];
             int tau = tau0;
             int st = 0, ui = 0, tl0 = 0, off = 0;
             if (tau < tau1) {
@@ -1363,7 +1394,7 @@ __global__ void __launch_bounds__(256, 1) k_upward_tc(LevelParams L, LevelParams
                 int st2 = 0, ui2 = 0, tl02 = 0, off2 = 0;
                 if (gend < tau1) {
                     decode(gend, st2, ui2, tl02, off2);
-                    load_b(st2, ui2, bn);
+                    if constexpr (C::PREFETCH) load_b(st2, ui2, bn);
                 }
                 const int p0 = pst[ui], p1 = pst[ui + 1];
                 for (int tile = tl0 + off; tile < tl0 + off + (gend - tau); ++tile) {
@@ -1409,8 +1440,12 @@ __global__ void __launch_bounds__(256, 1) k_upward_tc(LevelParams L, LevelParams
                     ui = ui2;
                     tl0 = tl02;
                     off = off2;
+                    if constexpr (C::PREFETCH) {
 #pragma unroll
-                    for (int ks = 0; ks < KS; ++ks) bc[ks] = bn[ks];
+                        for (int ks = 0; ks < KS; ++ks) bc[ks] = bn[ks];
+                    } else {
+                        load_b(st, ui, bc);
+                    }
                 }
             }
         } else {
@@ -1433,6 +1468,8 @@ __global__ void __launch_bounds__(256, 1) k_upward_tc(LevelParams L, LevelParams
                 sV[j * P + n] = acc;
             }
         }
+        if (phase_clk && lane == 0 && U <= umax)  // per-warp busy cycles of the task loop
+            atomicAdd(phase_clk + 8, (unsigned long long)(clock64() - t_task0));
         __syncthreads();
         mark(5);
     }
@@ -1489,6 +1526,379 @@ __global__ void __launch_bounds__(256, 1) k_upward_tc(LevelParams L, LevelParams
     mark(6);
 }
 
+// ---------------------------------------------------------------------------
+// K7 on the FP64 tensor core, v2 (P = 75, (P_s, P_ang) = (3, 5)): as k_upward_tc,
+// but without the per-octant tensor-basis matrix in shared memory.  The K index
+// of the DMMA is permuted so that every lane can form its own A fragments in
+// registers from the three 1-D Chebyshev vectors of its node:
+//   k' = 4 ks + tig,  ks < 15:  (a, b, c) = (ks % 3, ks / 3, tig)
+//                     ks >= 15: j = 4 (ks - 15) + tig, (a, b, c) = (j % 3, j / 3, 4)
+// (j = 15 is padding), i.e. coefficient index i = 15 tig + ks, resp. 60 + j: the
+// B fragments are plain strided loads of the child coefficient vectors.  Freed
+// shared memory (48.6 KB) lets two blocks share an SM, so one block's barriers
+// and geometry overlap the other's DMMAs.  Tasks per octant = (node-tile run of
+// one child cell, segment tile), contiguous per warp so consecutive tasks reuse
+// the A fragments.
+template <int PS, int PA>
+struct Tc2Cfg {
+    static_assert(PS == 3 && PA == 5, "k-permutation is specific to (P_s, P_ang) = (3, 5)");
+    static constexpr int P = 75, KS = 19, NR = 10, NW = 80;
+    static constexpr int J = kChunkTC2;
+    static constexpr int UM = 8;
+    static constexpr int NT = 256;
+    static constexpr int NWARP = NT / 32;
+    static constexpr int R = (NW + 31) / 32;
+    static constexpr int FG = 8;  // fit group (aliases the geometry)
+    static constexpr size_t a16(size_t x) { return (x + 15) / 16 * 16; }
+    static constexpr size_t oV = 0;                                       // double2 [J][P]
+    static constexpr size_t oG = a16(oV + (size_t)J * P * 16);            // double [8][NW][5]
+    static constexpr size_t oU = a16(oG + (size_t)8 * NW * 5 * 8);        // int [8][NW]
+    static constexpr size_t oSlot = a16(oU + (size_t)8 * NW * 4);         // int [8][UM][J]
+    static constexpr size_t oChild = a16(oSlot + (size_t)8 * UM * J * 4); // int [8][J]
+    static constexpr size_t oSeg = a16(oChild + (size_t)8 * J * 4);       // int [J]
+    static constexpr size_t oUcell = a16(oSeg + (size_t)J * 4);           // int [8][UM]
+    static constexpr size_t oMisc = a16(oUcell + (size_t)8 * UM * 4);     // int U[8], nO[8]
+    static constexpr size_t oPst = a16(oMisc + 16 * 4);                   // u8 [8][UM + 1]
+    static constexpr size_t oOrd = a16(oPst + (size_t)8 * (UM + 1));      // u8 [8][NW]
+    static constexpr size_t oUis = a16(oOrd + (size_t)8 * NW);            // u8 [8][NW]
+    static constexpr size_t oJl = a16(oUis + (size_t)8 * NW);             // u8 [8][J]
+    static constexpr size_t oFit = a16(oJl + (size_t)8 * J);              // double Ms, Ma
+    static constexpr size_t smem = a16(oFit + (size_t)(PS * PS + PA * PA) * 8);
+    static_assert(2 * FG * P * 16 <= 8 * NW * 5 * 8, "fit temporaries alias the geometry");
+};
+
+template <int PS, int PA>
+__global__ void __launch_bounds__(256, 2) k_upward_tc2(LevelParams L, LevelParams LP,
+                                                       const double2* __restrict__ vals_d, double k,
+                                                       const double* __restrict__ Ms, const double* __restrict__ Ma,
+                                                       double2* vals_p, int* bad, int umax,
+                                                       const double2* __restrict__ zseg) {
+    using C = Tc2Cfg<PS, PA>;
+    constexpr int P = C::P, KS = C::KS, NW = C::NW, J = C::J, UM = C::UM, NT = C::NT, NWARP = C::NWARP,
+                  R = C::R, FG = C::FG;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sV = reinterpret_cast<double2*>(smraw + C::oV);
+    double* sG = reinterpret_cast<double*>(smraw + C::oG);
+    int* sU = reinterpret_cast<int*>(smraw + C::oU);
+    int* sSlot = reinterpret_cast<int*>(smraw + C::oSlot);
+    int* sChild = reinterpret_cast<int*>(smraw + C::oChild);
+    int* sSeg = reinterpret_cast<int*>(smraw + C::oSeg);
+    int* sUcell = reinterpret_cast<int*>(smraw + C::oUcell);
+    int* sUn = reinterpret_cast<int*>(smraw + C::oMisc);
+    int* sNo = sUn + 8;
+    unsigned char* sPst = smraw + C::oPst;
+    unsigned char* sOrd = smraw + C::oOrd;
+    unsigned char* sUis = smraw + C::oUis;
+    unsigned char* sJl = smraw + C::oJl;
+    double* sMs = reinterpret_cast<double*>(smraw + C::oFit);
+    double* sMa = sMs + PS * PS;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t c = blockIdx.x;
+    const int s0 = LP.chunk_start[c];
+    const int s1 = (c + 1 < LP.nchunk) ? LP.chunk_start[c + 1] : (int)LP.nseg;
+    const int cnt = min(J, s1 - s0);
+
+    // ---- phase 0: segments, children by octant, per-octant compaction
+    for (int j = tid; j < J; j += NT) sSeg[j] = j < cnt ? LP.cell_seg[s0 + j] : -1;
+    for (int t = tid; t < PS * PS; t += NT) sMs[t] = Ms[t];
+    for (int t = tid; t < PA * PA; t += NT) sMa[t] = Ma[t];
+    for (int t = tid; t < J * P; t += NT) sV[t] = make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int t = tid; t < 8 * J; t += NT) {
+        const int o = t / J, j = t - o * J;
+        const int seg = sSeg[j];
+        int B = -1;
+        if (seg >= 0) {
+            B = LP.child_oct[8 * LP.seg_box[seg] + o];
+            if (B < L.b0 || B >= L.b1) B = -1;
+        }
+        sChild[t] = B;
+    }
+    __syncthreads();
+    {
+        const int o = warp;
+        int base = 0;
+        for (int j0 = 0; j0 < J; j0 += 32) {
+            const int j = j0 + lane;
+            const bool pr = j < J && sChild[o * J + j] >= 0;
+            const unsigned b = __ballot_sync(~0u, pr);
+            if (pr) sJl[o * J + base + __popc(b & lt)] = (unsigned char)j;
+            base += __popc(b);
+        }
+        if (lane == 0) sNo[o] = base;
+    }
+    __syncthreads();
+
+    // ---- phase 1: geometry of (octant, node)
+    const int cellp = LP.seg_cell[sSeg[0]];
+    const double hh = 0.5 * L.H;
+    for (int t = tid; t < 8 * NW; t += NT) {
+        const int o = t / NW, n = t - o * NW;
+        int u = INT_MAX;
+        if (n < P && sNo[o] > 0) {
+            double off[3];
+            node_off(LP, PS, PA, cellp, n, off);
+            const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
+            const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
+            const Cls cl = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+            u = (int)cell_of(L, cl);
+            // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
+            const double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
+            const double diff = num / (cl.r + rQ);
+            const double ratio = rQ / cl.r;
+            double sn, cs;
+            fm::sincos(k * diff, &sn, &cs);
+            double* g = sG + (size_t)t * 5;
+            g[0] = cl.us;
+            g[1] = cl.ut;
+            g[2] = cl.up;
+            g[3] = ratio * cs;
+            g[4] = ratio * sn;
+        }
+        sU[t] = u;
+    }
+    __syncthreads();
+
+    // ---- phase 2: per octant (warp): distinct child cells ascending, stable node
+    // sort by cell; cell index ui owns sorted positions [pst[ui], pst[ui + 1])
+    {
+        const int o = warp;
+        int uv[R];
+        bool done[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int n = lane + 32 * r;
+            uv[r] = n < NW ? sU[o * NW + n] : INT_MAX;
+            done[r] = !(n < P) || uv[r] == INT_MAX;
+        }
+        int base = 0, U = 0;
+        while (true) {
+            int m = INT_MAX;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (!done[r]) m = min(m, uv[r]);
+            m = __reduce_min_sync(~0u, m);
+            if (m == INT_MAX) break;
+            if (lane == 0 && U <= UM) sPst[o * (UM + 1) + U] = (unsigned char)base;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool hit = !done[r] && uv[r] == m;
+                const unsigned b = __ballot_sync(~0u, hit);
+                if (hit) {
+                    const int pos = base + __popc(b & lt);
+                    sOrd[o * NW + pos] = (unsigned char)(lane + 32 * r);
+                    sUis[o * NW + pos] = (unsigned char)min(U, 254);
+                    done[r] = true;
+                }
+                base += __popc(b);
+            }
+            if (lane == 0 && U < UM) sUcell[o * UM + U] = m;
+            ++U;
+        }
+        if (lane == 0 && U <= UM) sPst[o * (UM + 1) + U] = (unsigned char)base;
+        for (int pos = base + lane; pos < NW; pos += 32) {
+            sOrd[o * NW + pos] = (unsigned char)pos;
+            sUis[o * NW + pos] = 0xFF;
+        }
+        if (lane == 0) sUn[o] = U;
+    }
+    __syncthreads();
+
+    // ---- phase 3: child segment slots per (octant, cell, compacted segment)
+    for (int t = tid; t < 8 * UM * J; t += NT) {
+        const int o = t / (UM * J), rem = t - o * (UM * J), ui = rem / J, q = rem - ui * J;
+        int sl = -1;
+        if (ui < sUn[o] && sUn[o] <= umax && q < sNo[o]) {
+            const int B = sChild[o * J + sJl[o * J + q]];
+            const int64_t s64 = seg_slot(L, B, sUcell[o * UM + ui]);
+            if (s64 < 0) atomicOr(bad, 1);
+            sl = (int)s64;
+        }
+        sSlot[t] = sl;
+    }
+    __syncthreads();
+
+    // ---- phase 4: per octant, DMMA tasks (run of one cell's node tiles x segment tile)
+    const int gid = lane >> 2, tig = lane & 3;
+    // B fragment offsets of this lane (permuted k): i = 15 tig + ks (ks < 15), 60 + 4 (ks - 15) + tig
+    for (int o = 0; o < 8; ++o) {
+        const int no = sNo[o];
+        if (no == 0) continue;
+        const int U = sUn[o];
+        const double* g0 = sG + (size_t)o * NW * 5;
+        if (U <= umax) {
+            const unsigned char* pst = sPst + o * (UM + 1);
+            const int nst = (no + 7) >> 3;
+            // runs: (cell ui, node tile) in sorted order; tasks = runs x segment tiles
+            int nrun = 0;
+            for (int u = 0; u < U; ++u) nrun += ((pst[u + 1] - 1) >> 3) - (pst[u] >> 3) + 1;
+            const int T = nrun * nst;
+            const int tau0 = (int)((int64_t)warp * T / NWARP), tau1 = (int)((int64_t)(warp + 1) * T / NWARP);
+            int cur_run = -1, ui = 0, tile = 0;
+            double a[KS];
+            int run = tau0 / nst, st = tau0 - (tau0 / nst) * nst;
+            for (int tau = tau0; tau < tau1; ++tau) {
+                if (run != cur_run) {
+                    cur_run = run;
+                    int rr = run;
+                    ui = 0;
+                    while (true) {
+                        const int a0 = pst[ui] >> 3, n_t = ((pst[ui + 1] - 1) >> 3) - a0 + 1;
+                        if (rr < n_t) {
+                            tile = a0 + rr;
+                            break;
+                        }
+                        rr -= n_t;
+                        ++ui;
+                    }
+                    // A fragments of row (node) pos = 8 tile + gid in registers
+                    const int pos = tile * 8 + gid;
+                    const int nn = pos < P ? sOrd[o * NW + pos] : 0;
+                    const double* g = g0 + nn * 5;
+                    double Ts[3], Tt[5], Tp[5];
+                    cheb_T<3>(g[0], Ts);
+                    cheb_T<5>(g[1], Tt);
+                    cheb_T<5>(g[2], Tp);
+                    const double tpo = tig == 0 ? Tp[0] : (tig == 1 ? Tp[1] : (tig == 2 ? Tp[2] : Tp[3]));
+                    double tt[15];
+#pragma unroll
+                    for (int b = 0; b < 5; ++b)
+#pragma unroll
+                        for (int aa = 0; aa < 3; ++aa) tt[b * 3 + aa] = Ts[aa] * Tt[b];
+#pragma unroll
+                    for (int ks = 0; ks < 15; ++ks) a[ks] = tt[ks] * tpo;
+                    // ks = 15..18: j = 4 (ks - 15) + tig, product index j (j = 15: padding)
+                    const double t4 = Tp[4];
+                    a[15] = (tig == 0 ? tt[0] : (tig == 1 ? tt[1] : (tig == 2 ? tt[2] : tt[3]))) * t4;
+                    a[16] = (tig == 0 ? tt[4] : (tig == 1 ? tt[5] : (tig == 2 ? tt[6] : tt[7]))) * t4;
+                    a[17] = (tig == 0 ? tt[8] : (tig == 1 ? tt[9] : (tig == 2 ? tt[10] : tt[11]))) * t4;
+                    a[18] = (tig == 0 ? tt[12] : (tig == 1 ? tt[13] : (tig == 2 ? tt[14] : 0.0))) * t4;
+                }
+                // B fragments: column q = st*8 + gid
+                const int q = st * 8 + gid;
+                const int sl = sSlot[(o * UM + ui) * J + q];
+                const double2* cp = sl >= 0 ? vals_d + (int64_t)sl * P : zseg;
+                double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
+                double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
+                {
+                    double2 b[KS];
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) b[ks] = __ldg(cp + (ks < 15 ? 15 * tig + ks : 60 + 4 * (ks - 15) + tig));
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) {
+                        if (ks & 1) {
+                            dmma(er0, er1, a[ks], b[ks].x);
+                            dmma(ei0, ei1, a[ks], b[ks].y);
+                        } else {
+                            dmma(dr0, dr1, a[ks], b[ks].x);
+                            dmma(di0, di1, a[ks], b[ks].y);
+                        }
+                    }
+                }
+                const int pos = tile * 8 + gid;
+                if (pos >= pst[ui] && pos < pst[ui + 1]) {
+                    dr0 += er0;
+                    dr1 += er1;
+                    di0 += ei0;
+                    di1 += ei1;
+                    const int n = sOrd[o * NW + pos];
+                    const double rr = g0[n * 5 + 3], ri = g0[n * 5 + 4];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int qq = st * 8 + 2 * tig + h;
+                        if (qq < no) {
+                            const int j = sJl[o * J + qq];
+                            const double fr = h ? dr1 : dr0, fi = h ? di1 : di0;
+                            double2 acc = sV[j * P + n];
+                            acc.x = fma(rr, fr, fma(-ri, fi, acc.x));
+                            acc.y = fma(rr, fi, fma(ri, fr, acc.y));
+                            sV[j * P + n] = acc;
+                        }
+                    }
+                }
+                if (++st == nst) {
+                    st = 0;
+                    ++run;
+                }
+            }
+        } else {
+            // more distinct child cells than staged (near the poles): per (segment, node)
+            for (int t = tid; t < no * P; t += NT) {
+                const int q = t / P, n = t - q * P;
+                const int j = sJl[o * J + q];
+                const int B = sChild[o * J + j];
+                const double* g = g0 + n * 5;
+                const int64_t sl = seg_slot(L, B, sU[o * NW + n]);
+                if (sl < 0) {
+                    atomicOr(bad, 1);
+                    continue;
+                }
+                double Ts[PS], Tt[PA];
+                cheb_T<PS>(g[0], Ts);
+                cheb_T<PA>(g[1], Tt);
+                const double2 F = contract_sm_lr<PS, PA, true>(vals_d + sl * P, Ts, Tt, g[2]);
+                double2 acc = sV[j * P + n];
+                acc.x = fma(g[3], F.x, fma(-g[4], F.y, acc.x));
+                acc.y = fma(g[3], F.y, fma(g[4], F.x, acc.y));
+                sV[j * P + n] = acc;
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- phase 5: fused K5 fit (reading R1), groups of FG segments, three
+    // separable passes through the (now free) geometry buffer
+    double2* TA = reinterpret_cast<double2*>(sG);
+    double2* TB = TA + FG * P;
+    for (int j0 = 0; j0 < cnt; j0 += FG) {
+        const int nj = min(FG, cnt - j0);
+        for (int t = tid; t < nj * P; t += NT) {  // along s
+            const int jj = t / P, i = t - jj * P;
+            const int ia = i % PS, rest = i / PS;
+            const double2* v = sV + (j0 + jj) * P + rest * PS;
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int qq = 0; qq < PS; ++qq) {
+                const double m = sMs[ia * PS + qq];
+                xr = fma(m, v[qq].x, xr);
+                xi = fma(m, v[qq].y, xi);
+            }
+            TA[t] = make_double2(xr, xi);
+        }
+        __syncthreads();
+        for (int t = tid; t < nj * P; t += NT) {  // along theta
+            const int jj = t / P, i = t - jj * P;
+            const int ia = i % PS, ib = (i / PS) % PA, ic = i / (PS * PA);
+            const double2* v = TA + jj * P + ic * PA * PS + ia;
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int qq = 0; qq < PA; ++qq) {
+                const double m = sMa[ib * PA + qq];
+                xr = fma(m, v[qq * PS].x, xr);
+                xi = fma(m, v[qq * PS].y, xi);
+            }
+            TB[t] = make_double2(xr, xi);
+        }
+        __syncthreads();
+        for (int t = tid; t < nj * P; t += NT) {  // along phi
+            const int jj = t / P, i = t - jj * P;
+            const int ab = i % (PS * PA), ic = i / (PS * PA);
+            const double2* v = TB + jj * P + ab;
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int qq = 0; qq < PA; ++qq) {
+                const double m = sMa[ic * PA + qq];
+                xr = fma(m, v[qq * PS * PA].x, xr);
+                xi = fma(m, v[qq * PS * PA].y, xi);
+            }
+            vals_p[(int64_t)sSeg[j0 + jj] * P + i] = make_double2(xr, xi);
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------- dispatch
 template <int PS, int PA>
 struct Kern {
@@ -1505,6 +1915,20 @@ struct Kern {
     // returns true if the kernel also produced the Chebyshev coefficients (fused K5)
     static bool upward(dim3 g, cudaStream_t st, const LevelParams& L, const LevelParams& LP, const ifgf_plan_s* p,
                        const double2* vd, double2* vp, int* bad) {
+        if constexpr (PS == 3 && PA == 5) {
+            if (LP.up_kernel == 3 && LP.nchunk > 0) {
+                using Cfg = Tc2Cfg<PS, PA>;
+                static bool attr = false;
+                if (!attr) {
+                    IFGF_CUDA(cudaFuncSetAttribute(k_upward_tc2<PS, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)Cfg::smem));
+                    attr = true;
+                }
+                k_upward_tc2<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(
+                    L, LP, vd, p->k, p->cheb_Ms, p->cheb_Ma, vp, bad, std::min(Cfg::UM, p->tc_umax), p->zseg);
+                return true;
+            }
+        }
         if constexpr (PS > 0 && PS * PA * PA <= 80) {
             if (LP.up_kernel == 1 && LP.nchunk > 0) {
                 using Cfg = TcCfg<PS, PA>;
@@ -1681,7 +2105,9 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
         for (int i = 0; i < 7; ++i) tot += (double)h[i];
         fprintf(stderr, "[ifgf] TC K7 phase clocks (block-thread-0 sums, %% of total %.3g):", tot);
         for (int i = 0; i < 7; ++i) fprintf(stderr, " p%d=%.1f%%", i, 100.0 * (double)h[i] / (tot > 0 ? tot : 1));
-        fprintf(stderr, "\n");
+        fprintf(stderr, "; task-loop warp utilisation %.1f%% (%d warps)\n",
+                100.0 * (double)h[8] / ((double)TcCfg<3, 5>::NWARP * (double)(h[5] > 0 ? h[5] : 1)),
+                TcCfg<3, 5>::NWARP);
     }
     {
         Prof pr(p, st, 6);

@@ -879,19 +879,22 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         }
         S.release(keys_in);
         // K7 kernel by mean segments per cell run (measured on B200):
-        // many -> FP64 tensor-core GEMM; some -> cell-grouped staged DFMA; ~1-2 ->
-        // per-evaluation geometry (nothing to share, least overhead)
-        int kern = per_run >= 24.0 ? 1 : (per_run >= 6.0 ? 0 : 2);
+        // many -> FP64 tensor-core GEMM (64-chunks, basis in shared memory); some ->
+        // register-basis tensor-core GEMM (32-chunks, 2 blocks/SM) for (3, 5), else the
+        // cell-grouped staged DFMA kernel; ~1-2 -> per-evaluation geometry
+        int kern = per_run >= 24.0 ? 1 : (per_run >= 6.0 ? ((Ps == 3 && Pa == 5) ? 3 : 0) : 2);
         if (p->legacy_upward == 1 || p->legacy_upward == 7) kern = 2;  // per-evaluation (1: per-lane loads)
         if (p->legacy_upward >= 2 && p->legacy_upward <= 4) kern = 0;  // 16-chunk variants
         if (p->legacy_upward == 5) kern = 1;                           // force the tensor-core kernel
+        if (p->legacy_upward == 8) kern = 3;                           // force the tensor-core kernel v2
         if (P > 80 && kern == 1) kern = 0;  // TC kernel shared memory is sized for P <= 80 ((P_s, P_ang) = (3, 5))
-        const int tc = kern == 1;
+        if (kern == 3 && !(Ps == 3 && Pa == 5)) kern = 1;  // TC v2 k-permutation is specific to (3, 5)
+        const int tc = kern == 1 || kern == 3;
         L.p.up_kernel = kern;
         if (std::getenv("IFGF_PLAN_VERBOSE"))
             fprintf(stderr, "[ifgf] level %d: %lld segments, %lld cell runs, %.2f per run, tile %.0f MB, K7 kernel %d\n",
                     d, (long long)ns, (long long)nrun, per_run, tile_bytes / 1e6, kern);
-        k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, tc ? kChunkTC : kChunk, flag);
+        k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, kern == 3 ? kChunkTC2 : (tc ? kChunkTC : kChunk), flag);
         inclusive_scan(S, flag, incl, ns, st);
         int64_t nch = d2h_one(incl + ns - 1, st);
         L.chunk_start = dev_alloc<int>(p, nch);
