@@ -532,83 +532,6 @@ __global__ void __launch_bounds__(TPB, 4) k_upward(LevelParams L, LevelParams LP
     vals_p[sp * P + n] = make_double2(ar, ai);
 }
 
-// K7, cell-grouped: the child-relative geometry of a parent node (child cell,
-// local coordinates, recentering factor) depends only on (cell gamma', node,
-// child octant), not on the box.  One block per chunk of <= kChunk parent
-// segments that share gamma' (thread = node): the geometry of each octant is
-// computed once and reused for every segment of the chunk; all threads of the
-// block evaluate the same child box at the same time (L1-broadcast loads).
-template <int PS, int PA>
-__global__ void __launch_bounds__(128, 4) k_upward_g(LevelParams L, LevelParams LP, const double2* __restrict__ vals_d,
-                                                  double k, double2* vals_p, int* bad) {
-    constexpr int P = PS * PA * PA;
-    constexpr int CH = kChunk;
-    constexpr int NT = ((P + 31) / 32) * 32;
-    __shared__ int sh_seg[CH];
-    __shared__ int sh_child[CH][8];
-    __shared__ unsigned sh_omask;
-    __shared__ double2 sh_acc[CH][NT];
-    const int64_t c = blockIdx.x;
-    const int s0 = LP.chunk_start[c];
-    const int s1 = (c + 1 < LP.nchunk) ? LP.chunk_start[c + 1] : (int)LP.nseg;
-    const int cnt = min(CH, s1 - s0);
-    if (threadIdx.x == 0) sh_omask = 0u;
-    __syncthreads();
-    for (int t = threadIdx.x; t < CH * 8; t += blockDim.x) {
-        int j = t >> 3, o = t & 7;
-        int B = -1;
-        if (j < cnt) {
-            int seg = LP.cell_seg[s0 + j];
-            if (o == 0) sh_seg[j] = seg;
-            B = LP.child_oct[8 * LP.seg_box[seg] + o];
-            if (B < L.b0 || B >= L.b1) B = -1;
-            if (B >= 0) atomicOr(&sh_omask, 1u << o);
-        }
-        sh_child[j][o] = B;
-    }
-    __syncthreads();
-    const int n = threadIdx.x;
-    if (n >= P) return;
-    const unsigned omask = sh_omask;
-    double off[3];
-    node_off(LP, PS, PA, LP.seg_cell[sh_seg[0]], n, off);
-    const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
-    const double hh = 0.5 * L.H;
-    for (int j = 0; j < cnt; ++j) sh_acc[j][n] = make_double2(0.0, 0.0);
-    for (int o = 0; o < 8; ++o) {
-        if (!((omask >> o) & 1u)) continue;
-        const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
-        Cls cl = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
-        const int64_t cell = cell_of(L, cl);
-        double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
-        double diff = num / (cl.r + rQ);
-        double ratio = rQ / cl.r;
-        double sn, cs;
-        fm::sincos(k * diff, &sn, &cs);
-        const double rr = ratio * cs, ri = ratio * sn;
-        double Ts[PS], Tt[PA];
-        cheb_T<PS>(cl.us, Ts);
-        cheb_T<PA>(cl.ut, Tt);
-        const double up = cl.up;
-#pragma unroll 1
-        for (int j = 0; j < cnt; ++j) {
-            const int B = sh_child[j][o];
-            if (B < 0) continue;
-            const int64_t slot = seg_slot(L, B, cell);
-            if (slot < 0) {
-                atomicOr(bad, 1);
-                continue;
-            }
-            double2 F = contract<PS, PA>(vals_d + slot * P, Ts, Tt, up);
-            double2 acc = sh_acc[j][n];
-            acc.x = fma(rr, F.x, fma(-ri, F.y, acc.x));
-            acc.y = fma(rr, F.y, fma(ri, F.x, acc.y));
-            sh_acc[j][n] = acc;
-        }
-    }
-    for (int j = 0; j < cnt; ++j) vals_p[(int64_t)sh_seg[j] * P + n] = sh_acc[j][n];
-}
-
 // ---------------------------------------------------------------------------
 // K7, cell-grouped + shared-memory staged.  Per (chunk, octant) the nodes of
 // the block map to a handful (U) of child cells; those U child segments are
@@ -832,248 +755,12 @@ __global__ void __launch_bounds__(128, 3) k_upward_s(LevelParams L, LevelParams 
     }
 }
 
-// ---------------------------------------------------------------------------
-// K7 on the FP64 tensor core.  Within a chunk (<= 16 parent segments sharing
-// cone cell gamma') and octant o, the per-node geometry is shared, so
-//   V[j][n] += rec_n * sum_i C[B_j, c_n][i] * w_n[i]     (w_n = tensor basis)
-// is, for each child cell u, a dense (segments x coefficients) x
-// (coefficients x nodes of u) product: DMMA m8n8k4 tiles with rows = segments,
-// cols = nodes (sorted by child cell; columns of other cells get weight 0),
-// k = coefficient index.  Real and imaginary parts are two MMAs sharing the
-// weight fragment.  A fragments come straight from global (L1/L2), weights from
-// shared memory.
+// FP64 tensor-core MMA: D(8x8) += A(8x4) B(4x8), lane holds A[gid][tig], B[tig][gid],
+// D[gid][2 tig + {0,1}] (gid = lane / 4, tig = lane % 4).
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
-}
-
-template <int PS, int PA>
-struct MmaCfg {
-    static constexpr int P = PS * PA * PA;
-    static constexpr int KS = (P + 3) / 4;          // k-steps
-    static constexpr int NW = ((P + 7) / 8) * 8;    // weight columns (node slots)
-    static constexpr int NWP = (NW % 16 == 0) ? NW + 4 : NW;  // row stride: 4 k-rows cover each bank twice (2 wavefronts)
-    static constexpr int NT = 128;                  // threads (4 warps)
-    static constexpr size_t smem = (size_t)(4 * KS) * NWP * sizeof(double) + (size_t)kChunk * P * sizeof(double2);
-};
-
-template <int PS, int PA>
-__global__ void __launch_bounds__(128, 2) k_upward_mma(LevelParams L, LevelParams LP,
-                                                       const double2* __restrict__ vals_d, double k,
-                                                       const double* __restrict__ Ms, const double* __restrict__ Ma,
-                                                       double2* vals_p, int* bad) {
-    using Cfg = MmaCfg<PS, PA>;
-    constexpr int P = Cfg::P, KS = Cfg::KS, NW = Cfg::NW, NWP = Cfg::NWP, NT = Cfg::NT, CH = kChunk;
-    extern __shared__ double dsm2[];
-    double* sh_w = dsm2;  // [4*KS][NWP] weights, cell-sorted columns
-    double2* sh_acc = reinterpret_cast<double2*>(dsm2 + 4 * KS * NWP);  // [CH][P] by node
-    __shared__ int sh_seg[CH];
-    __shared__ int sh_child[CH][8];
-    __shared__ unsigned sh_omask;
-    __shared__ int sh_cell[NW];    // child cell of node n
-    __shared__ int sh_order[NW];   // node at sorted column
-    __shared__ int sh_ccol[NW];    // child cell of sorted column (-1 pad)
-    __shared__ double2 sh_rec[NW];
-    __shared__ int sh_task[NW];    // (tile << 8) | (first column of the cell run in the tile)
-    __shared__ int sh_ntask;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int gid = lane >> 2, tig = lane & 3;
-    const int64_t c = blockIdx.x;
-    const int s0 = LP.chunk_start[c];
-    const int s1 = (c + 1 < LP.nchunk) ? LP.chunk_start[c + 1] : (int)LP.nseg;
-    const int cnt = min(CH, s1 - s0);
-    if (tid == 0) sh_omask = 0u;
-    __syncthreads();
-    for (int t = tid; t < CH * 8; t += NT) {
-        int j = t >> 3, o = t & 7;
-        int B = -1;
-        if (j < cnt) {
-            int seg = LP.cell_seg[s0 + j];
-            if (o == 0) sh_seg[j] = seg;
-            B = LP.child_oct[8 * LP.seg_box[seg] + o];
-            if (B < L.b0 || B >= L.b1) B = -1;
-            if (B >= 0) atomicOr(&sh_omask, 1u << o);
-        }
-        sh_child[j][o] = B;
-    }
-    for (int t = tid; t < CH * P; t += NT) sh_acc[t] = make_double2(0.0, 0.0);
-    __syncthreads();
-    const int n = tid;
-    const bool active = n < P;
-    const unsigned omask = sh_omask;
-    double off[3] = {0.0, 0.0, 0.0};
-    if (active) node_off(LP, PS, PA, LP.seg_cell[sh_seg[0]], n, off);
-    const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
-    const double hh = 0.5 * L.H;
-    const int mtiles = (cnt + 7) >> 3;
-    for (int o = 0; o < 8; ++o) {
-        if (!((omask >> o) & 1u)) continue;
-        const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
-        double Ts[PS], Tt[PA], Tp[PA];
-        int cellc = 0x7fffffff;
-        if (active) {
-            Cls cl = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
-            cellc = (int)cell_of(L, cl);
-            double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
-            double diff = num / (cl.r + rQ);
-            double ratio = rQ / cl.r;
-            double sn, cs;
-            fm::sincos(k * diff, &sn, &cs);
-            sh_rec[n] = make_double2(ratio * cs, ratio * sn);
-            cheb_T<PS>(cl.us, Ts);
-            cheb_T<PA>(cl.ut, Tt);
-            cheb_T<PA>(cl.up, Tp);
-        }
-        if (n < NW) sh_cell[n] = cellc;
-        __syncthreads();
-        // stable sort of the nodes by child cell -> column position
-        int pos = 0;
-        if (active) {
-            for (int m = 0; m < P; ++m) {
-                const int cm = sh_cell[m];
-                pos += (cm < cellc) || (cm == cellc && m < n);
-            }
-            sh_order[pos] = n;
-            sh_ccol[pos] = cellc;
-        } else if (n < NW) {
-            sh_ccol[n] = -1;  // padding columns P..NW-1
-        }
-        __syncthreads();
-        // weights w_n[i] = Ts[a] Tt[b] Tp[c], i = (c*PA + b)*PS + a, at column pos(n)
-        if (active) {
-            for (int cc = 0; cc < PA; ++cc)
-                for (int b = 0; b < PA; ++b) {
-                    const double tb = Tt[b] * Tp[cc];
-#pragma unroll
-                    for (int a = 0; a < PS; ++a) sh_w[((cc * PA + b) * PS + a) * NWP + pos] = Ts[a] * tb;
-                }
-        }
-        for (int t = tid; t < (4 * KS - P) * NWP; t += NT) sh_w[P * NWP + t] = 0.0;  // k padding rows
-        // tasks: (8-column tile, cell run inside the tile)
-        if (tid == 0) {
-            int nt = 0;
-            for (int tile = 0; tile < NW / 8; ++tile)
-                for (int col = tile * 8; col < tile * 8 + 8; ++col) {
-                    const int cc = sh_ccol[col];
-                    if (cc < 0) break;
-                    if (col == tile * 8 || cc != sh_ccol[col - 1]) sh_task[nt++] = (tile << 8) | col;
-                }
-            sh_ntask = nt;
-        }
-        __syncthreads();
-        const int ntask = sh_ntask;
-        for (int t = warp; t < ntask * mtiles; t += NT / 32) {
-            const int task = sh_task[t % ntask], mt = t / ntask;
-            const int tile = task >> 8, col0 = task & 0xff;
-            const int u = sh_ccol[col0];
-            const int col = tile * 8 + gid;  // this lane's B column
-            const bool colok = sh_ccol[col] == u;
-            // A row of this lane: segment j = mt*8 + gid
-            const int j = mt * 8 + gid;
-            const double2* arow = nullptr;
-            if (j < cnt) {
-                const int B = sh_child[j][o];
-                if (B >= 0) {
-                    const int64_t slot = seg_slot(L, B, u);
-                    if (slot < 0) atomicOr(bad, 1);
-                    else arow = vals_d + slot * P;
-                }
-            }
-            // all A fragments of the task are loaded up front (one latency per task)
-            double2 av[KS];
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks) {
-                const int kk = 4 * ks + tig;
-                av[ks] = (arow && kk < P) ? __ldg(arow + kk) : make_double2(0.0, 0.0);
-            }
-            // even / odd k-steps accumulate separately: 4 independent DMMA chains
-            double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
-            double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks) {
-                const int kk = 4 * ks + tig;
-                const double bw = colok ? sh_w[kk * NWP + col] : 0.0;
-                if (ks & 1) {
-                    dmma(er0, er1, av[ks].x, bw);
-                    dmma(ei0, ei1, av[ks].y, bw);
-                } else {
-                    dmma(dr0, dr1, av[ks].x, bw);
-                    dmma(di0, di1, av[ks].y, bw);
-                }
-            }
-            dr0 += er0;
-            dr1 += er1;
-            di0 += ei0;
-            di1 += ei1;
-            // D[j'][c'] at j' = mt*8 + gid, columns tile*8 + 2*tig + {0,1}
-            const int jo = mt * 8 + gid;
-            if (jo < cnt && sh_child[jo][o] >= 0) {
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int cq = tile * 8 + 2 * tig + q;
-                    if (sh_ccol[cq] != u) continue;
-                    const int nn = sh_order[cq];
-                    const double2 rc = sh_rec[nn];
-                    const double fr = q ? dr1 : dr0, fi = q ? di1 : di0;
-                    double2 acc = sh_acc[jo * P + nn];
-                    acc.x = fma(rc.x, fr, fma(-rc.y, fi, acc.x));
-                    acc.y = fma(rc.x, fi, fma(rc.y, fr, acc.y));
-                    sh_acc[jo * P + nn] = acc;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    // Fused K5 fit (as in k_upward_s); temporaries reuse the weight buffer.
-    double ms[PS], mt_[PA], mp[PA];
-    const int ia = n % PS, ib = (n / PS) % PA, ic = n / (PS * PA);
-    if (active) {
-#pragma unroll
-        for (int q = 0; q < PS; ++q) ms[q] = __ldg(Ms + ia * PS + q);
-#pragma unroll
-        for (int q = 0; q < PA; ++q) {
-            mt_[q] = __ldg(Ma + ib * PA + q);
-            mp[q] = __ldg(Ma + ic * PA + q);
-        }
-    }
-    double2* tA = reinterpret_cast<double2*>(sh_w);
-    double2* tB = tA + P;
-    for (int j = 0; j < cnt; ++j) {
-        const double2* V = sh_acc + j * P;
-        if (active) {
-            double xr = 0.0, xi = 0.0;
-#pragma unroll
-            for (int q = 0; q < PS; ++q) {
-                double2 v = V[(ic * PA + ib) * PS + q];
-                xr = fma(ms[q], v.x, xr);
-                xi = fma(ms[q], v.y, xi);
-            }
-            tA[n] = make_double2(xr, xi);
-        }
-        __syncthreads();
-        if (active) {
-            double xr = 0.0, xi = 0.0;
-#pragma unroll
-            for (int q = 0; q < PA; ++q) {
-                double2 v = tA[(ic * PA + q) * PS + ia];
-                xr = fma(mt_[q], v.x, xr);
-                xi = fma(mt_[q], v.y, xi);
-            }
-            tB[n] = make_double2(xr, xi);
-        }
-        __syncthreads();
-        if (active) {
-            double xr = 0.0, xi = 0.0;
-#pragma unroll
-            for (int q = 0; q < PA; ++q) {
-                double2 v = tB[(q * PA + ib) * PS + ia];
-                xr = fma(mp[q], v.x, xr);
-                xi = fma(mp[q], v.y, xi);
-            }
-            vals_p[(int64_t)sh_seg[j] * P + n] = make_double2(xr, xi);
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1943,27 +1630,8 @@ struct Kern {
                     p->phase_clk);
                 return true;
             }
-            // FP64 tensor-core kernel on 16-chunks (A/B variant 4)
-            if (LP.up_kernel == 0 && p->legacy_upward == 4 && LP.nchunk > 0) {
-                using Cfg = MmaCfg<PS, PA>;
-                static bool attr = false;
-                if (!attr) {
-                    IFGF_CUDA(cudaFuncSetAttribute(k_upward_mma<PS, PA>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem));
-                    attr = true;
-                }
-                k_upward_mma<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(L, LP, vd, p->k, p->cheb_Ms,
-                                                                                        p->cheb_Ma, vp, bad);
-                return true;
-            }
         }
         if constexpr (PS > 0 && PS * PA * PA <= 128) {
-            if (LP.up_kernel == 0 && LP.nchunk > 0 && p->legacy_upward == 2) {
-                constexpr int P = PS * PA * PA;
-                const int threads = ((P + 31) / 32) * 32;
-                k_upward_g<PS, PA><<<(unsigned)LP.nchunk, threads, 0, st>>>(L, LP, vd, p->k, vp, bad);
-                return false;
-            }
             if (LP.up_kernel == 0 && LP.nchunk > 0) {
                 using Cfg = StagedCfg<PS, PA>;
                 static bool attr = false;

@@ -884,7 +884,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         // cell-grouped staged DFMA kernel; ~1-2 -> per-evaluation geometry
         int kern = per_run >= 24.0 ? 1 : (per_run >= 6.0 ? ((Ps == 3 && Pa == 5) ? 3 : 0) : 2);
         if (p->legacy_upward == 1 || p->legacy_upward == 7) kern = 2;  // per-evaluation (1: per-lane loads)
-        if (p->legacy_upward >= 2 && p->legacy_upward <= 4) kern = 0;  // 16-chunk variants
+        if (p->legacy_upward == 3) kern = 0;                           // staged DFMA everywhere
         if (p->legacy_upward == 5) kern = 1;                           // force the tensor-core kernel
         if (p->legacy_upward == 8) kern = 3;                           // force the tensor-core kernel v2
         if (P > 80 && kern == 1) kern = 0;  // TC kernel shared memory is sized for P <= 80 ((P_s, P_ang) = (3, 5))

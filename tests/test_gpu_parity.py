@@ -248,18 +248,17 @@ def test_cfg2_parity(ifgf):
     assert oracle.rel_l2(got[tg], exact) <= 1.1 * oracle.rel_l2(ref[tg], exact)
 
 
-@pytest.mark.parametrize("mode,umax", [("1", None), ("2", None), ("3", None), ("4", None), ("5", None),
-                                       ("5", "1"), ("5", "0"), ("7", None), ("8", None), ("8", "1")])
+@pytest.mark.parametrize("mode,umax", [("1", None), ("3", None), ("5", None), ("5", "1"), ("5", "0"), ("7", None),
+                                       ("8", None), ("8", "1")])
 def test_upward_kernel_variants(ifgf, mode, umax, monkeypatch):
-    """Every K7 variant (1 per-evaluation geometry, 2 cell-grouped, 3 cell-grouped
-    + shared-memory staged, 4 FP64 tensor-core DMMA on 16-chunks, 5 the FP64
-    tensor-core GEMM kernel on 64-chunks at every level, 7 the warp-staged
-    per-evaluation kernel at every level, 8 the register-basis tensor-core
-    kernel on 32-chunks at every level) matches the oracle.
-    IFGF_TC_UMAX caps the child cells the TC kernel stages per octant, so that its
-    per-node fallback (taken near the poles) is exercised too.  The default (0)
-    picks the TC kernel where many segments share a cell, the staged kernel where
-    some do, the per-evaluation kernel where ~1-2 do."""
+    """Every K7 kernel forced at every level matches the oracle (env
+    IFGF_LEGACY_UPWARD: 1 per-evaluation geometry with per-lane global loads,
+    3 cell-grouped shared-memory staged DFMA, 5 FP64 tensor-core GEMM on
+    64-chunks, 7 warp-staged per-evaluation, 8 register-basis FP64 tensor-core
+    GEMM on 32-chunks).  IFGF_TC_UMAX caps the child cells the tensor-core
+    kernels stage per octant, so that their per-node fallback (taken near the
+    poles) is exercised too.  The default (0) picks per level by segments per
+    cell run."""
     monkeypatch.setenv("IFGF_LEGACY_UPWARD", mode)
     if umax is not None:
         monkeypatch.setenv("IFGF_TC_UMAX", umax)
