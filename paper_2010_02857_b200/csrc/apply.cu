@@ -33,6 +33,37 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// Bulk (TMA) copies global -> shared completing on an mbarrier (sm_90+ async proxy):
+// one instruction per contiguous segment instead of one 16-byte cp.async per lane.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    unsigned ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
 __global__ void k_permute(const double2* __restrict__ in, const int* __restrict__ perm, int64_t n, double2* out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) out[i] = in[perm[i]];
@@ -307,9 +338,16 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
     constexpr int SMAX = P <= 80 ? 4 : 2;  // static shared memory <= 48 KB per block
     constexpr int SP = P + 2;  // slot stride (double2): 4 slots -> disjoint banks for 16-byte reads
     __shared__ __align__(16) double2 sbuf[TPB / 32][2][SMAX][SP];
+    __shared__ __align__(8) unsigned long long sbar[TPB / 32][2];
     const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (item >= L.nwitems) return;  // warp-uniform
+    if (lane == 0) {
+        mbar_init(&sbar[w][0], 1);
+        mbar_init(&sbar[w][1], 1);
+    }
+    __syncwarp();
+    unsigned phase = 0u;  // bit b: parity of buffer b's next completion
     const int2 it = L.witems[item];
     const int T = it.x, l = it.y + lane;
     const bool active = l < L.box_start[T + 1];
@@ -322,6 +360,7 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
     auto prep = [&](int e, CousinEv<PS, PA>& v, int buf) {
         v.slot = -1;
         v.bi = -1;
+        int nd = 0;
         const int B = L.cou_idx[e];
         if (B >= L.b0 && B < L.b1) {
             const double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
@@ -340,33 +379,28 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
                 v.up = c.up;
             }
             unsigned pend = __ballot_sync(~0u, v.slot >= 0);
-            int nd = 0;
+            if (lane == 0) fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
             while (pend && nd < SMAX) {
                 const int leader = __ffs(pend) - 1;
                 const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
-                const double2* src = vals + s0 * P;
-                double2* dst = &sbuf[w][buf][nd][0];
-                for (int i = lane; i < P; i += 32) cp_async16(dst + i, src + i);
+                if (lane == 0) bulk_g2s(&sbuf[w][buf][nd][0], vals + s0 * P, P * sizeof(double2), &sbar[w][buf]);
                 const bool mine = v.slot == s0;
                 if (mine) v.bi = nd;
                 pend &= ~__ballot_sync(~0u, mine);
                 ++nd;
             }
         }
-        cp_async_commit();
+        if (lane == 0) mbar_arrive_expect_tx(&sbar[w][buf], (unsigned)(nd * P * sizeof(double2)));
     };
     double ar = 0.0, ai = 0.0;
     const int e0 = L.cou_off[T], e1 = L.cou_off[T + 1];
     CousinEv<PS, PA> cur, nxt;
     if (e0 < e1) prep(e0, cur, 0);
     for (int e = e0; e < e1; ++e) {
-        if (e + 1 < e1) {
-            prep(e + 1, nxt, (e + 1 - e0) & 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncwarp();
+        if (e + 1 < e1) prep(e + 1, nxt, (e + 1 - e0) & 1);
+        const int cb = (e - e0) & 1;
+        mbar_wait(&sbar[w][cb], (phase >> cb) & 1u);
+        phase ^= 1u << cb;
         if (cur.slot >= 0) {
             const double2 F = cur.bi >= 0
                                   ? contract_sm_lr<PS, PA>(&sbuf[w][(e - e0) & 1][cur.bi][0], cur.Ts, cur.Tt, cur.up)
@@ -399,9 +433,16 @@ __global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams
     constexpr int SMAX = P <= 80 ? 4 : 2;
     constexpr int SP = P + 2;
     __shared__ __align__(16) double2 sbuf[TPB / 32][2][SMAX][SP];
+    __shared__ __align__(8) unsigned long long sbar[TPB / 32][2];
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if ((t & ~(int64_t)31) >= LP.nseg * P) return;  // warp-uniform
+    if (lane == 0) {
+        mbar_init(&sbar[w][0], 1);
+        mbar_init(&sbar[w][1], 1);
+    }
+    __syncwarp();
+    unsigned phase = 0u;  // bit b: parity of buffer b's next completion
     const bool active = t < LP.nseg * P;
     const int64_t sp = active ? t / P : 0;
     const int n = active ? (int)(t - sp * P) : 0;
@@ -443,31 +484,26 @@ __global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams
         }
         unsigned pend = __ballot_sync(~0u, v.slot >= 0);
         int nd = 0;
+        if (lane == 0) fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
         while (pend && nd < SMAX) {
             const int leader = __ffs(pend) - 1;
             const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
-            const double2* src = vals_d + s0 * P;
-            double2* dst = &sbuf[w][buf][nd][0];
-            for (int i = lane; i < P; i += 32) cp_async16(dst + i, src + i);
+            if (lane == 0) bulk_g2s(&sbuf[w][buf][nd][0], vals_d + s0 * P, P * sizeof(double2), &sbar[w][buf]);
             const bool mine = v.slot == s0;
             if (mine) v.bi = nd;
             pend &= ~__ballot_sync(~0u, mine);
             ++nd;
         }
-        cp_async_commit();
+        if (lane == 0) mbar_arrive_expect_tx(&sbar[w][buf], (unsigned)(nd * P * sizeof(double2)));
     };
     double ar = 0.0, ai = 0.0;
     Ev cur, nxt;
     prep(0, cur, 0);
 #pragma unroll 1
     for (int o = 0; o < 8; ++o) {
-        if (o + 1 < 8) {
-            prep(o + 1, nxt, (o + 1) & 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncwarp();
+        if (o + 1 < 8) prep(o + 1, nxt, (o + 1) & 1);
+        mbar_wait(&sbar[w][o & 1], (phase >> (o & 1)) & 1u);
+        phase ^= 1u << (o & 1);
         if (cur.slot >= 0) {
             double Ts[PS], Tt[PA];
             cheb_T<PS>(cur.us, Ts);
@@ -992,7 +1028,8 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
         }
         sSlot[t] = sl;
     }
-    __syncthreads();
+    // (no barrier: the first octant's basis build below does not read the slots,
+    // and its closing barrier orders them before the first DMMA task)
     mark(3);
 
     // ---- phase 4: per octant, W_o then DMMA tasks
