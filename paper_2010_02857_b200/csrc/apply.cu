@@ -64,6 +64,16 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
     } while (!ok);
 }
 
+// 1/x for x > 0 (values only): hardware approximation + two Newton steps (~1 ulp).
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
 __global__ void k_permute(const double2* __restrict__ in, const int* __restrict__ perm, int64_t n, double2* out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) out[i] = in[perm[i]];
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(TPB) k_s2c(LevelParams L, const double* __rest
                                              double2* vals) {
     const int P = Ps * Pa * Pa;
     int64_t B = L.b0 + blockIdx.x;
-    __shared__ double sw[S2C_CHUNK][3];
+    __shared__ double sw[S2C_CHUNK][4];  // source - centre (x, y, z), |source - centre|^2
     __shared__ double2 sa[S2C_CHUNK];
     const int64_t row = (B - L.b0) * L.W;
     const int64_t s0 = L.rank[row], s1 = L.rank[row + L.W];
@@ -183,22 +193,24 @@ __global__ void __launch_bounds__(TPB) k_s2c(LevelParams L, const double* __rest
             int cn = min(S2C_CHUNK, m1 - c0);
             __syncthreads();
             for (int t = threadIdx.x; t < cn; t += blockDim.x) {
-                sw[t][0] = px[c0 + t] - cx;
-                sw[t][1] = py[c0 + t] - cy;
-                sw[t][2] = pz[c0 + t] - cz;
+                const double wx = px[c0 + t] - cx, wy = py[c0 + t] - cy, wz = pz[c0 + t] - cz;
+                sw[t][0] = wx;
+                sw[t][1] = wy;
+                sw[t][2] = wz;
+                sw[t][3] = fma(wx, wx, fma(wy, wy, wz * wz));
                 sa[t] = a[c0 + t];
             }
             __syncthreads();
             if (active) {
                 for (int t = 0; t < cn; ++t) {
-                    double wx = sw[t][0], wy = sw[t][1], wz = sw[t][2];
-                    double dx = off[0] - wx, dy = off[1] - wy, dz = off[2] - wz;
+                    const double wx = sw[t][0], wy = sw[t][1], wz = sw[t][2], ww = sw[t][3];
+                    const double dx = off[0] - wx, dy = off[1] - wy, dz = off[2] - wz;
                     const double d2 = fma(dx, dx, fma(dy, dy, dz * dz));
                     const double rdi = rsqrt(d2);
                     const double rd = d2 * rdi;
                     // |y - x_m| - |y - c| = (w.w - 2 off.w) / (|off - w| + |off|)   (reading R17)
-                    double num = fma(wx, wx, fma(wy, wy, wz * wz)) - 2.0 * fma(off[0], wx, fma(off[1], wy, off[2] * wz));
-                    double diff = num * __drcp_rn(rd + ro);
+                    const double num = fma(-2.0, fma(off[0], wx, fma(off[1], wy, off[2] * wz)), ww);
+                    const double diff = num * rcp_nr(rd + ro);
                     double ratio = ro * rdi;
                     double sn, cs;
                     fm::sincos(k * diff, &sn, &cs);
@@ -371,7 +383,7 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
                 if (v.slot < 0) atomicOr(bad, 1);
                 double sn, cs;
                 fm::sincos(k * c.r, &sn, &cs);
-                const double wr = kInv4Pi / c.r;
+                const double wr = kInv4Pi * rcp_nr(c.r);
                 v.gr = cs * wr;
                 v.gi = sn * wr;
                 cheb_T<PS>(c.us, v.Ts);
@@ -472,8 +484,9 @@ __global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams
             // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
             const double num =
                 fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
-            const double diff = num / (c.r + rQ);
-            const double ratio = rQ / c.r;
+            const double ic = rcp_nr(c.r * (c.r + rQ));
+            const double diff = num * c.r * ic;
+            const double ratio = rQ * (c.r + rQ) * ic;
             double sn, cs;
             fm::sincos(k * diff, &sn, &cs);
             v.rr = ratio * cs;
@@ -952,8 +965,9 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
             u = (int)cell_of(L, cl);
             // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
             const double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
-            const double diff = num / (cl.r + rQ);
-            const double ratio = rQ / cl.r;
+            const double ic = rcp_nr(cl.r * (cl.r + rQ));
+            const double diff = num * cl.r * ic;
+            const double ratio = rQ * (cl.r + rQ) * ic;
             double sn, cs;
             fm::sincos(k * diff, &sn, &cs);
             double* g = sG + (size_t)t * 5;
@@ -1370,8 +1384,9 @@ __global__ void __launch_bounds__(256, 2) k_upward_tc2(LevelParams L, LevelParam
             u = (int)cell_of(L, cl);
             // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
             const double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
-            const double diff = num / (cl.r + rQ);
-            const double ratio = rQ / cl.r;
+            const double ic = rcp_nr(cl.r * (cl.r + rQ));
+            const double diff = num * cl.r * ic;
+            const double ratio = rQ * (cl.r + rQ) * ic;
             double sn, cs;
             fm::sincos(k * diff, &sn, &cs);
             double* g = sG + (size_t)t * 5;

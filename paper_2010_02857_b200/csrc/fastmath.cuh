@@ -111,7 +111,19 @@ IFGF_HD double atan2(double y, double x) {
     const double ax = std::fabs(x), ay = std::fabs(y);
     const double mx = std::fmax(ax, ay), mn = std::fmin(ax, ay);
     const bool big = mn > kTanPi8 * mx;  // reduce via atan(t) = pi/4 + atan((t-1)/(t+1))
-    const double t = (big ? mn - mx : mn) / (big ? mn + mx : mx);
+    const double num = big ? mn - mx : mn, den = big ? mn + mx : mx;
+#ifdef __CUDA_ARCH__
+    // value only: hardware reciprocal + two Newton steps (~1 ulp) instead of an IEEE division
+    double rd;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(den));
+    double e = std::fma(-den, rd, 1.0);
+    rd = std::fma(rd, e, rd);
+    e = std::fma(-den, rd, 1.0);
+    rd = std::fma(rd, e, rd);
+    const double t = num * rd;
+#else
+    const double t = num / den;
+#endif
     const double s = t * t;
     double q = IFGF_FMC(kAtanQ, 0);
     q = std::fma(q, s, IFGF_FMC(kAtanQ, 1));
