@@ -94,7 +94,7 @@ struct LevelParams {  // passed by value to kernels
 };
 
 constexpr int kChunk = 16;
-constexpr int kChunkTC = 64;
+constexpr int kChunkTC = 96;
 constexpr int kChunkTC2 = 32;
 
 struct LevelHost {
