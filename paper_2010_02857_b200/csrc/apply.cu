@@ -345,7 +345,7 @@ template <int PS, int PA>
 __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const double* __restrict__ px,
                                                    const double* __restrict__ py, const double* __restrict__ pz,
                                                    const double2* __restrict__ vals, double k, double2* out,
-                                                   int* bad) {
+                                                   int* bad, int smax) {
     constexpr int P = PS * PA * PA;
     constexpr int SMAX = P <= 80 ? 4 : 2;  // static shared memory <= 48 KB per block
     constexpr int SP = P + 2;  // slot stride (double2): 4 slots -> disjoint banks for 16-byte reads
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
             }
             unsigned pend = __ballot_sync(~0u, v.slot >= 0);
             if (lane == 0) fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
-            while (pend && nd < SMAX) {
+            while (pend && nd < min(SMAX, smax)) {
                 const int leader = __ffs(pend) - 1;
                 const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
                 if (lane == 0) bulk_g2s(&sbuf[w][buf][nd][0], vals + s0 * P, P * sizeof(double2), &sbar[w][buf]);
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
 template <int PS, int PA>
 __global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams LP,
                                                       const double2* __restrict__ vals_d, double k, double2* vals_p,
-                                                      int* bad) {
+                                                      int* bad, int smax) {
     constexpr int P = PS * PA * PA;
     constexpr int SMAX = P <= 80 ? 4 : 2;
     constexpr int SP = P + 2;
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams
         unsigned pend = __ballot_sync(~0u, v.slot >= 0);
         int nd = 0;
         if (lane == 0) fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
-        while (pend && nd < SMAX) {
+        while (pend && nd < min(SMAX, smax)) {
             const int leader = __ffs(pend) - 1;
             const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
             if (lane == 0) bulk_g2s(&sbuf[w][buf][nd][0], vals_d + s0 * P, P * sizeof(double2), &sbar[w][buf]);
@@ -1645,7 +1645,7 @@ struct Kern {
                        double2* out, int* bad) {
         if constexpr (PS > 0) {
             if (!p->legacy_cousin) {
-                k_cousin_ws<PS, PA><<<g, TPB, 0, st>>>(L, p->px, p->py, p->pz, v, p->k, out, bad);
+                k_cousin_ws<PS, PA><<<g, TPB, 0, st>>>(L, p->px, p->py, p->pz, v, p->k, out, bad, p->stage_slots);
                 return;
             }
         }
@@ -1699,7 +1699,7 @@ struct Kern {
         }
         if constexpr (PS > 0) {
             if (p->legacy_upward != 1) {
-                k_upward_pe<PS, PA><<<g, TPB, 0, st>>>(L, LP, vd, p->k, vp, bad);
+                k_upward_pe<PS, PA><<<g, TPB, 0, st>>>(L, LP, vd, p->k, vp, bad, p->stage_slots);
                 return false;
             }
         }

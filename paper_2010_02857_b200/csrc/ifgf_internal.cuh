@@ -153,6 +153,7 @@ struct ifgf_plan_s {
     int* dev_bad = nullptr;  // device flag: apply-time invariant violation (EINTERNAL)
     int legacy_upward = 0;   // env IFGF_LEGACY_UPWARD: K7 variant override (A/B testing, tests)
     int tc_umax = 1 << 30;
+    int stage_slots = 1 << 30;  // env IFGF_STAGE_SLOTS: cap on staged child segments per warp in K6 / K7-pe (tests)
     int legacy_cousin = 0;   // env IFGF_LEGACY_COUSIN=1: per-lane global-load K6 (A/B testing)
     unsigned long long* phase_clk = nullptr;  // env IFGF_PHASE_PROF: TC K7 per-phase clock sums   // env IFGF_TC_UMAX: cap on staged child cells in the TC K7 (tests the fallback)
     int64_t device_bytes = 0;

@@ -204,11 +204,16 @@ def test_multirank_emulation_one_gpu(ifgf):
         assert oracle.rel_l2(acc, full) < 1e-13, R
 
 
-@pytest.mark.parametrize("legacy", ["0", "1"])
-def test_cousin_kernel_variants(ifgf, legacy, monkeypatch):
+@pytest.mark.parametrize("legacy,slots", [("0", None), ("0", "1"), ("0", "0"), ("1", None)])
+def test_cousin_kernel_variants(ifgf, legacy, slots, monkeypatch):
     """K6: the warp-staged kernel (default) and the per-lane global-load kernel
-    (IFGF_LEGACY_COUSIN=1) both match the oracle."""
+    (IFGF_LEGACY_COUSIN=1) both match the oracle.  IFGF_STAGE_SLOTS caps the child
+    segments a warp stages (K6 and the per-evaluation K7), so that their
+    global-memory fallback is exercised as well."""
     monkeypatch.setenv("IFGF_LEGACY_COUSIN", legacy)
+    if slots is not None:
+        monkeypatch.setenv("IFGF_STAGE_SLOTS", slots)
+        monkeypatch.setenv("IFGF_LEGACY_UPWARD", "7")
     n = 20000
     pts = inputs.rough_sphere(n)
     a = inputs.densities(n, seed=8)
