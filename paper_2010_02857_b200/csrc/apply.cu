@@ -812,6 +812,91 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// K5 fit of cnt segments' node values held in shared memory, IN PLACE (reading R1):
+// three separable passes, each thread transforming whole 1-D lines (P_s values
+// along s, P_ang along theta / phi) in registers, so no temporary buffer and only
+// three barriers; the phi pass writes the coefficients to out[seg[j] * P + i].
+template <int PS, int PA>
+__device__ __forceinline__ void fit_lines_inplace(double2* V, int cnt, const int* seg, const double* Ms,
+                                                  const double* Ma, double2* out, int tid, int nt) {
+    constexpr int P = PS * PA * PA;
+    double ms[PS * PS], ma[PA * PA];
+#pragma unroll
+    for (int i = 0; i < PS * PS; ++i) ms[i] = __ldg(Ms + i);
+#pragma unroll
+    for (int i = 0; i < PA * PA; ++i) ma[i] = __ldg(Ma + i);
+    __syncthreads();
+    for (int t = tid; t < cnt * PA * PA; t += nt) {  // along s: line (j, b, c)
+        const int j = t / (PA * PA), bc = t - j * (PA * PA);
+        double2* v = V + j * P + bc * PS;
+        double2 x[PS];
+#pragma unroll
+        for (int q = 0; q < PS; ++q) x[q] = v[q];
+#pragma unroll
+        for (int a = 0; a < PS; ++a) {
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int q = 0; q < PS; ++q) {
+                xr = fma(ms[a * PS + q], x[q].x, xr);
+                xi = fma(ms[a * PS + q], x[q].y, xi);
+            }
+            v[a] = make_double2(xr, xi);
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < cnt * PS * PA; t += nt) {  // along theta: line (j, a, c)
+        const int j = t / (PS * PA), r = t - j * (PS * PA), c = r / PS, a = r - c * PS;
+        double2* v = V + j * P + c * PA * PS + a;
+        double2 x[PA];
+#pragma unroll
+        for (int q = 0; q < PA; ++q) x[q] = v[q * PS];
+#pragma unroll
+        for (int b = 0; b < PA; ++b) {
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int q = 0; q < PA; ++q) {
+                xr = fma(ma[b * PA + q], x[q].x, xr);
+                xi = fma(ma[b * PA + q], x[q].y, xi);
+            }
+            v[b * PS] = make_double2(xr, xi);
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < cnt * PS * PA; t += nt) {  // along phi: line (j, a, b) -> global
+        const int j = t / (PS * PA), ab = t - j * (PS * PA);
+        const double2* v = V + j * P + ab;
+        double2 x[PA];
+#pragma unroll
+        for (int q = 0; q < PA; ++q) x[q] = v[q * PS * PA];
+        double2* o = out + (int64_t)seg[j] * P + ab;
+#pragma unroll
+        for (int c = 0; c < PA; ++c) {
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int q = 0; q < PA; ++q) {
+                xr = fma(ma[c * PA + q], x[q].x, xr);
+                xi = fma(ma[c * PA + q], x[q].y, xi);
+            }
+            o[c * PS * PA] = make_double2(xr, xi);
+        }
+    }
+}
+
+// K5 for the levels whose K7 writes node values (per-evaluation kernel, leaf):
+// block = 8 consecutive segments staged in shared memory, in-place line passes.
+template <int PS, int PA>
+__global__ void __launch_bounds__(128) k_fit_lines(int64_t nseg, const double* __restrict__ Ms,
+                                                   const double* __restrict__ Ma, double2* vals) {
+    constexpr int P = PS * PA * PA, NSB = 8;
+    __shared__ double2 sv[NSB * P];
+    __shared__ int sseg[NSB];
+    const int64_t s0 = (int64_t)blockIdx.x * NSB;
+    const int cnt = (int)min((int64_t)NSB, nseg - s0);
+    for (int t = threadIdx.x; t < cnt * P; t += blockDim.x) sv[t] = vals[s0 * P + t];
+    if (threadIdx.x < NSB) sseg[threadIdx.x] = (int)(s0 + threadIdx.x);
+    fit_lines_inplace<PS, PA>(sv, cnt, sseg, Ms, Ma, vals, threadIdx.x, blockDim.x);
+}
+
 // ---------------------------------------------------------------------------
 // K7 on the FP64 tensor core, large cell chunks (fine levels).
 //
@@ -1212,56 +1297,8 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
         mark(5);
     }
 
-    // ---- phase 5: fused K5 fit (reading R1), groups of FG segments, three
-    // separable passes through the (now free) W buffer
-    double2* TA = reinterpret_cast<double2*>(sW);
-    double2* TB = TA + FG * P;
-    for (int j0 = 0; j0 < cnt; j0 += FG) {
-        const int nj = min(FG, cnt - j0);
-        for (int t = tid; t < nj * P; t += NT) {  // along s
-            const int jj = t / P, i = t - jj * P;
-            const int ia = i % PS, rest = i / PS;
-            const double2* v = sV + (j0 + jj) * P + rest * PS;
-            double xr = 0.0, xi = 0.0;
-#pragma unroll
-            for (int q = 0; q < PS; ++q) {
-                const double m = sMs[ia * PS + q];
-                xr = fma(m, v[q].x, xr);
-                xi = fma(m, v[q].y, xi);
-            }
-            TA[t] = make_double2(xr, xi);
-        }
-        __syncthreads();
-        for (int t = tid; t < nj * P; t += NT) {  // along theta
-            const int jj = t / P, i = t - jj * P;
-            const int ia = i % PS, ib = (i / PS) % PA, ic = i / (PS * PA);
-            const double2* v = TA + jj * P + ic * PA * PS + ia;
-            double xr = 0.0, xi = 0.0;
-#pragma unroll
-            for (int q = 0; q < PA; ++q) {
-                const double m = sMa[ib * PA + q];
-                xr = fma(m, v[q * PS].x, xr);
-                xi = fma(m, v[q * PS].y, xi);
-            }
-            TB[t] = make_double2(xr, xi);
-        }
-        __syncthreads();
-        for (int t = tid; t < nj * P; t += NT) {  // along phi
-            const int jj = t / P, i = t - jj * P;
-            const int ab = i % (PS * PA), ic = i / (PS * PA);
-            const double2* v = TB + jj * P + ab;
-            double xr = 0.0, xi = 0.0;
-#pragma unroll
-            for (int q = 0; q < PA; ++q) {
-                const double m = sMa[ic * PA + q];
-                xr = fma(m, v[q * PS * PA].x, xr);
-                xi = fma(m, v[q * PS * PA].y, xi);
-            }
-            vals_p[(int64_t)sSeg[j0 + jj] * P + i] = make_double2(xr, xi);
-        }
-        __syncthreads();
-    }
-    mark(6);
+    // ---- phase 5: fused K5 fit, in place, three barriers
+    fit_lines_inplace<PS, PA>(sV, cnt, sSeg, Ms, Ma, vals_p, tid, NT);
 }
 
 // ---------------------------------------------------------------------------
@@ -1587,55 +1624,8 @@ __global__ void __launch_bounds__(256, 2) k_upward_tc2(LevelParams L, LevelParam
         __syncthreads();
     }
 
-    // ---- phase 5: fused K5 fit (reading R1), groups of FG segments, three
-    // separable passes through the (now free) geometry buffer
-    double2* TA = reinterpret_cast<double2*>(sG);
-    double2* TB = TA + FG * P;
-    for (int j0 = 0; j0 < cnt; j0 += FG) {
-        const int nj = min(FG, cnt - j0);
-        for (int t = tid; t < nj * P; t += NT) {  // along s
-            const int jj = t / P, i = t - jj * P;
-            const int ia = i % PS, rest = i / PS;
-            const double2* v = sV + (j0 + jj) * P + rest * PS;
-            double xr = 0.0, xi = 0.0;
-#pragma unroll
-            for (int qq = 0; qq < PS; ++qq) {
-                const double m = sMs[ia * PS + qq];
-                xr = fma(m, v[qq].x, xr);
-                xi = fma(m, v[qq].y, xi);
-            }
-            TA[t] = make_double2(xr, xi);
-        }
-        __syncthreads();
-        for (int t = tid; t < nj * P; t += NT) {  // along theta
-            const int jj = t / P, i = t - jj * P;
-            const int ia = i % PS, ib = (i / PS) % PA, ic = i / (PS * PA);
-            const double2* v = TA + jj * P + ic * PA * PS + ia;
-            double xr = 0.0, xi = 0.0;
-#pragma unroll
-            for (int qq = 0; qq < PA; ++qq) {
-                const double m = sMa[ib * PA + qq];
-                xr = fma(m, v[qq * PS].x, xr);
-                xi = fma(m, v[qq * PS].y, xi);
-            }
-            TB[t] = make_double2(xr, xi);
-        }
-        __syncthreads();
-        for (int t = tid; t < nj * P; t += NT) {  // along phi
-            const int jj = t / P, i = t - jj * P;
-            const int ab = i % (PS * PA), ic = i / (PS * PA);
-            const double2* v = TB + jj * P + ab;
-            double xr = 0.0, xi = 0.0;
-#pragma unroll
-            for (int qq = 0; qq < PA; ++qq) {
-                const double m = sMa[ic * PA + qq];
-                xr = fma(m, v[qq * PS * PA].x, xr);
-                xi = fma(m, v[qq * PS * PA].y, xi);
-            }
-            vals_p[(int64_t)sSeg[j0 + jj] * P + i] = make_double2(xr, xi);
-        }
-        __syncthreads();
-    }
+    // ---- phase 5: fused K5 fit, in place, three barriers
+    fit_lines_inplace<PS, PA>(sV, cnt, sSeg, Ms, Ma, vals_p, tid, NT);
 }
 
 // ------------------------------------------------------------- dispatch
@@ -1781,8 +1771,14 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
         LevelParams& L = p->lev[d].p;
         if (L.nseg == 0) return;
         Prof pr(p, st, 3);
-        k_fit<<<(int)((L.nseg + fit_warps - 1) / fit_warps), 32 * fit_warps, fit_smem, st>>>(
-            L.nseg, Ps, Pa, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]);
+        const unsigned nb8 = (unsigned)((L.nseg + 7) / 8);
+        dispatch(
+            Ps, Pa, [&] { k_fit_lines<3, 5><<<nb8, 128, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
+            [&] { k_fit_lines<5, 5><<<nb8, 128, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
+            [&] {
+                k_fit<<<(int)((L.nseg + fit_warps - 1) / fit_warps), 32 * fit_warps, fit_smem, st>>>(
+                    L.nseg, Ps, Pa, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]);
+            });
         pr.done();
     };
     if (have) fit(D);
