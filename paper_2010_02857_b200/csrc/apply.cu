@@ -97,8 +97,13 @@ __global__ void __launch_bounds__(TPB) k_near(LevelParams L, const double* __res
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (item >= L.nwitems) return;  // warp-uniform
     const int2 it = L.witems[item];
-    const int T = it.x, l = it.y + lane;
-    const bool active = l < L.box_start[T + 1];
+    // items with <= 16 targets run split: lanes l and l + 16 take the same target
+    // and alternate sources; the halves are summed at the end (fixed order)
+    const int T = it.x, nT = min(32, L.box_start[T + 1] - it.y);
+    const bool split = nT <= 16;
+    const int half = split ? lane >> 4 : 0, step = split ? 2 : 1;
+    const int l = it.y + (split ? (lane & 15) : lane);
+    const bool active = l < it.y + nT;
     double x = 0.0, y = 0.0, z = 0.0;
     if (active) {
         x = px[l];
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(TPB) k_near(LevelParams L, const double* __res
             __syncwarp();
             if (active) {
 #pragma unroll 2
-                for (int t = 0; t < cn; ++t) {
+                for (int t = half; t < cn; t += step) {
                     if (c0 + t == l) continue;
                     const double dx = x - sx[w][t], dy = y - sy[w][t], dz = z - sz[w][t];
                     const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
@@ -140,7 +145,11 @@ __global__ void __launch_bounds__(TPB) k_near(LevelParams L, const double* __res
             }
         }
     }
-    if (active) out[l] = make_double2(ar, ai);
+    if (split) {
+        ar += __shfl_down_sync(~0u, ar, 16);
+        ai += __shfl_down_sync(~0u, ai, 16);
+    }
+    if (active && half == 0) out[l] = make_double2(ar, ai);
 }
 
 __device__ __forceinline__ void node_off(const LevelParams& LP, int Ps, int Pa, int cell, int n, double off[3]) {
@@ -361,69 +370,78 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
     __syncwarp();
     unsigned phase = 0u;  // bit b: parity of buffer b's next completion
     const int2 it = L.witems[item];
-    const int T = it.x, l = it.y + lane;
-    const bool active = l < L.box_start[T + 1];
+    // items with <= 16 targets run split: lanes l and l + 16 take the same target
+    // and alternate cousin boxes (per-lane B; the election spans both halves); the
+    // halves are summed at the end (fixed order)
+    const int T = it.x, nT = min(32, L.box_start[T + 1] - it.y);
+    const bool split = nT <= 16;
+    const int half = split ? lane >> 4 : 0, step = split ? 2 : 1;
+    const int l = it.y + (split ? (lane & 15) : lane);
+    const bool active = l < it.y + nT;
     double x = 0.0, y = 0.0, z = 0.0;
     if (active) {
         x = px[l];
         y = py[l];
         z = pz[l];
     }
-    auto prep = [&](int e, CousinEv<PS, PA>& v, int buf) {
+    const int e0 = L.cou_off[T], e1 = L.cou_off[T + 1];
+    auto prep = [&](int i, CousinEv<PS, PA>& v, int buf) {  // iteration i: cousin e0 + step i + half
         v.slot = -1;
         v.bi = -1;
         int nd = 0;
-        const int B = L.cou_idx[e];
-        if (B >= L.b0 && B < L.b1) {
+        const int e = e0 + step * i + half;
+        const int B = e < e1 ? L.cou_idx[e] : -1;
+        if (active && B >= L.b0 && B < L.b1) {
             const double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
                          cz = box_centre(L, L.box_ijk[3 * B + 2], 2);
-            if (active) {
-                const Cls c = classify(L, __dsub_rn(x, cx), __dsub_rn(y, cy), __dsub_rn(z, cz));
-                v.slot = seg_slot(L, B, cell_of(L, c));
-                if (v.slot < 0) atomicOr(bad, 1);
-                double sn, cs;
-                fm::sincos(k * c.r, &sn, &cs);
-                const double wr = kInv4Pi * rcp_nr(c.r);
-                v.gr = cs * wr;
-                v.gi = sn * wr;
-                cheb_T<PS>(c.us, v.Ts);
-                cheb_T<PA>(c.ut, v.Tt);
-                v.up = c.up;
-            }
-            unsigned pend = __ballot_sync(~0u, v.slot >= 0);
-            if (lane == 0) fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
-            while (pend && nd < min(SMAX, smax)) {
-                const int leader = __ffs(pend) - 1;
-                const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
-                if (lane == 0) bulk_g2s(&sbuf[w][buf][nd][0], vals + s0 * P, P * sizeof(double2), &sbar[w][buf]);
-                const bool mine = v.slot == s0;
-                if (mine) v.bi = nd;
-                pend &= ~__ballot_sync(~0u, mine);
-                ++nd;
-            }
+            const Cls c = classify(L, __dsub_rn(x, cx), __dsub_rn(y, cy), __dsub_rn(z, cz));
+            v.slot = seg_slot(L, B, cell_of(L, c));
+            if (v.slot < 0) atomicOr(bad, 1);
+            double sn, cs;
+            fm::sincos(k * c.r, &sn, &cs);
+            const double wr = kInv4Pi * rcp_nr(c.r);
+            v.gr = cs * wr;
+            v.gi = sn * wr;
+            cheb_T<PS>(c.us, v.Ts);
+            cheb_T<PA>(c.ut, v.Tt);
+            v.up = c.up;
+        }
+        unsigned pend = __ballot_sync(~0u, v.slot >= 0);
+        if (lane == 0) fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
+        while (pend && nd < min(SMAX, smax)) {
+            const int leader = __ffs(pend) - 1;
+            const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
+            if (lane == 0) bulk_g2s(&sbuf[w][buf][nd][0], vals + s0 * P, P * sizeof(double2), &sbar[w][buf]);
+            const bool mine = v.slot == s0;
+            if (mine) v.bi = nd;
+            pend &= ~__ballot_sync(~0u, mine);
+            ++nd;
         }
         if (lane == 0) mbar_arrive_expect_tx(&sbar[w][buf], (unsigned)(nd * P * sizeof(double2)));
     };
     double ar = 0.0, ai = 0.0;
-    const int e0 = L.cou_off[T], e1 = L.cou_off[T + 1];
+    const int niter = (e1 - e0 + step - 1) / step;
     CousinEv<PS, PA> cur, nxt;
-    if (e0 < e1) prep(e0, cur, 0);
-    for (int e = e0; e < e1; ++e) {
-        if (e + 1 < e1) prep(e + 1, nxt, (e + 1 - e0) & 1);
-        const int cb = (e - e0) & 1;
+    if (niter > 0) prep(0, cur, 0);
+    for (int i = 0; i < niter; ++i) {
+        if (i + 1 < niter) prep(i + 1, nxt, (i + 1) & 1);
+        const int cb = i & 1;
         mbar_wait(&sbar[w][cb], (phase >> cb) & 1u);
         phase ^= 1u << cb;
         if (cur.slot >= 0) {
-            const double2 F = cur.bi >= 0
-                                  ? contract_sm_lr<PS, PA>(&sbuf[w][(e - e0) & 1][cur.bi][0], cur.Ts, cur.Tt, cur.up)
-                                  : contract_sm_lr<PS, PA>(vals + cur.slot * P, cur.Ts, cur.Tt, cur.up);
+            const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA>(&sbuf[w][cb][cur.bi][0], cur.Ts, cur.Tt, cur.up)
+                                          : contract_sm_lr<PS, PA>(vals + cur.slot * P, cur.Ts, cur.Tt, cur.up);
             ar = fma(cur.gr, F.x, fma(-cur.gi, F.y, ar));
             ai = fma(cur.gr, F.y, fma(cur.gi, F.x, ai));
         }
-        __syncwarp();  // slot buffer (e & 1) is refilled by prep(e + 2)
+        __syncwarp();  // slot buffer (i & 1) is refilled by prep(i + 2)
         cur = nxt;
     }
-    if (active) {
+    if (split) {
+        ar += __shfl_down_sync(~0u, ar, 16);
+        ai += __shfl_down_sync(~0u, ai, 16);
+    }
+    if (active && half == 0) {
         const double2 o = out[l];
         out[l] = make_double2(o.x + ar, o.y + ai);
     }
