@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(TPB) k_near(LevelParams L, const double* __res
     __shared__ double2 sa[TPB / 32][32];
     const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (item >= L.nwitems) return;  // warp-uniform
-    const int2 it = L.witems[item];
+    if (item >= L.nwitems_near) return;  // warp-uniform
+    const int2 it = L.witems_near[item];
     // items with <= 16 targets run split: lanes l and l + 16 take the same target
     // and alternate sources; the halves are summed at the end (fixed order)
     const int T = it.x, nT = min(32, L.box_start[T + 1] - it.y);
@@ -1766,7 +1766,10 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
     LevelHost& LD = p->lev[D];
     if (mask & IFGF_STAGE_NEAR) {
         Prof pr(p, st, 1);
-        k_near<<<nblk(LD.p.nwitems * 32), TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, p->out_sorted);
+        if (p->nranks > 1)  // targets without an owned neighbour get no near-field work item
+            IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));
+        k_near<<<nblk(LD.p.nwitems_near * 32), TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k,
+                                                               p->out_sorted);
         pr.done();
     } else {
         IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));

@@ -75,9 +75,13 @@ struct LevelParams {  // passed by value to kernels
     const double* ct_tab;
     const double* sp_tab;     // 2 nC * Pa
     const double* cp_tab;
-    // K6 warp work items (box, first point)
+    // K6 warp work items (box, first point); multi-rank: only target boxes with an
+    // owned cousin (and cou_off / cou_idx filtered to owned boxes)
     const int2* witems;
     int64_t nwitems;
+    // K3 (leaf level) work items; multi-rank: target boxes with an owned neighbour
+    const int2* witems_near;
+    int64_t nwitems_near;
     // children of each box by octant ((i&1)<<2 | (j&1)<<1 | (k&1)) at level d + 1, -1 if absent
     const int* child_oct;
     // segments grouped by cone cell (box-independent K7 geometry): cell_seg = segment

@@ -436,6 +436,39 @@ T d2h_one(const T* p, cudaStream_t st) {
 }
 
 // CSR build from a count kernel: off = exclusive scan of counts (+ total).
+// Multi-rank: a rank only evaluates its own source boxes, so its target-major
+// kernels get neighbour / cousin lists filtered to owned boxes and work items only
+// for target boxes with at least one owned entry.
+__global__ void k_count_owned(const int* __restrict__ off, const int* __restrict__ idx, int64_t nb, int64_t b0,
+                              int64_t b1, int* cnt) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    int c = 0;
+    for (int e = off[b]; e < off[b + 1]; ++e) c += (idx[e] >= b0 && idx[e] < b1);
+    cnt[b] = c;
+}
+__global__ void k_emit_owned(const int* __restrict__ off, const int* __restrict__ idx, int64_t nb, int64_t b0,
+                             int64_t b1, const int* __restrict__ off2, int* idx2) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    int o = off2[b];
+    for (int e = off[b]; e < off[b + 1]; ++e)
+        if (idx[e] >= b0 && idx[e] < b1) idx2[o++] = idx[e];
+}
+__global__ void k_witem_count_masked(const int* __restrict__ start, int64_t nb, const int* __restrict__ own,
+                                     int* cnt) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    cnt[b] = own[b] > 0 ? (start[b + 1] - start[b] + 31) / 32 : 0;
+}
+__global__ void k_witem_fill_masked(const int* __restrict__ start, int64_t nb, const int* __restrict__ own,
+                                    const int* __restrict__ off, int2* items) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb || own[b] == 0) return;
+    int o = off[b];
+    for (int q = start[b]; q < start[b + 1]; q += 32) items[o++] = make_int2((int)b, q);
+}
+
 int* csr_offsets(ifgf_plan_s* p, Scratch& S, const int* cnt, int64_t n, cudaStream_t st, int64_t* total) {
     int* off = dev_alloc<int>(p, n + 1);
     int* incl = S.get<int>(n);
@@ -909,6 +942,45 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         S.release(rs);
         S.release(rsm);
         S.release(incl);
+    }
+
+    // 7c. multi-rank: owned-only neighbour / cousin lists and work items
+    if (p->nranks > 1) {
+        for (int d = 3; d <= D; ++d) {
+            LevelHost& L = p->lev[d];
+            const int64_t nb = L.p.nbox;
+            int* cnt = S.get<int>(nb);
+            int* wc = S.get<int>(nb);
+            auto filter = [&](const int* off, const int* idx, const int** off_out, const int** idx_out,
+                              const int2** items_out, int64_t* nitems_out) {
+                k_count_owned<<<nblocks(nb), TPB, 0, st>>>(off, idx, nb, L.p.b0, L.p.b1, cnt);
+                int64_t tot = 0;
+                int* off2 = csr_offsets(p, S, cnt, nb, st, &tot);
+                int* idx2 = dev_alloc<int>(p, tot);
+                k_emit_owned<<<nblocks(nb), TPB, 0, st>>>(off, idx, nb, L.p.b0, L.p.b1, off2, idx2);
+                k_witem_count_masked<<<nblocks(nb), TPB, 0, st>>>(L.box_start, nb, cnt, wc);
+                int64_t ni = 0;
+                int* woff = csr_offsets(p, S, wc, nb, st, &ni);
+                int2* items = dev_alloc<int2>(p, ni);
+                k_witem_fill_masked<<<nblocks(nb), TPB, 0, st>>>(L.box_start, nb, cnt, woff, items);
+                IFGF_CUDA(cudaGetLastError());
+                *off_out = off2;
+                *idx_out = idx2;
+                *items_out = items;
+                *nitems_out = ni;
+            };
+            filter(L.cou_off, L.cou_idx, &L.p.cou_off, &L.p.cou_idx, &L.p.witems, &L.p.nwitems);
+            if (d == D)
+                filter(L.nbr_off, L.nbr_idx, &L.p.nbr_off, &L.p.nbr_idx, &L.p.witems_near, &L.p.nwitems_near);
+            IFGF_CUDA(cudaStreamSynchronize(st));
+            S.release(cnt);
+            S.release(wc);
+        }
+    }
+    if (p->nranks == 1 || D < 3) {
+        LevelHost& LD = p->lev[D];
+        LD.p.witems_near = LD.p.witems;
+        LD.p.nwitems_near = LD.p.nwitems;
     }
 
     // 8. stats (algorithmic work units)
