@@ -763,10 +763,14 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             // work weight per leaf: points^2 (near + s2c proxy) + points * levels (cousin proxy)
             std::vector<int> starts(nleaf + 1);
             IFGF_CUDA(cudaMemcpy(starts.data(), LD.box_start, sizeof(int) * (nleaf + 1), cudaMemcpyDeviceToHost));
+            // work weight per leaf (ns on one B200, cfg4 per-unit costs):
+            // near field ~0.1 m^2 (m targets x ~14 neighbour leaves of similar size),
+            // source-to-cone + cousins ~(3.2 + 2.3 (D - 2)) m, and the upward passes of
+            // its ancestors ~100 (D - 2) per leaf independent of m (per-box cone data)
             std::vector<double> w(nleaf);
             for (int64_t b = 0; b < nleaf; ++b) {
-                double m = starts[b + 1] - starts[b];
-                w[b] = 14.0 * m * m + 8.0 * P * m + 45.0 * 4.0 * (D - 2) * m;
+                const double m = starts[b + 1] - starts[b];
+                w[b] = 0.1 * m * m + (3.2 + 2.3 * (D - 2)) * m * (P / 75.0) + 100.0 * (D - 2) * (P / 75.0);
             }
             std::vector<int64_t> bounds(p->nranks + 1);
             ifgf_status ps = ifgf_partition(w.data(), nleaf, p->nranks, bounds.data());
