@@ -124,19 +124,39 @@ def time_oracle_sample(repeats: int = 1):
     return c["n"], ts
 
 
+def workload_config(c, world: int, st=None) -> dict:
+    """The `config` object of the JSON line (same for both arms)."""
+    cfg = {
+        "workload": f"{c.name}: {c.geometry} {c.scale}, k={c.k / math.pi:.0f}pi ({c.k / math.pi:.0f} lambda across), "
+                    f"N={c.n}, D={c.levels}, (P_s,P_ang)=({c.Ps},{c.Pang}), Fibonacci points, "
+                    "splitmix64 densities",
+        "N": c.n, "k": c.k, "levels": c.levels, "P_s": c.Ps, "P_ang": c.Pang,
+        "parallelism": f"source-partition x{world} (Morton leaf ranges) + NCCL all-reduce" if world > 1
+        else "1 GPU",
+    }
+    if st is not None:
+        cfg["l2"] = ("inputs larger than L2: each apply streams "
+                     f"{sum(st['segment_bytes'].values()) / 1e9:.1f} GB of cone-segment data")
+    return cfg
+
+
 def run_reference(args, rank: int):
+    """Reference arm: the oracle (serial C++ CPU IFGF) timed as it stands on a bounded
+    sample of the same workload family (the full cfg4 apply would take ~35 min on one
+    core); the line carries our arm's config, metric and unit."""
     if rank != 0:
         return
     n, ts = time_oracle_sample(args.warmup + args.steps)
     timed = ts[args.warmup:] if len(ts) > args.warmup else ts
     t = sum(timed) / len(timed)
     value = n / t
+    sample = CPU_SAMPLE_DESC + f"; {len(timed)} timed applies after {args.warmup} warm-up"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CPU_SAMPLE_DESC},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": CPU_SAMPLE_DESC},
+        "config": workload_config(inputs.CONFIGS[args.config], 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -259,16 +279,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {
-                "workload": f"{c.name}: {c.geometry} {c.scale}, k={c.k / math.pi:.0f}pi ({c.k / math.pi:.0f} lambda across), "
-                            f"N={c.n}, D={c.levels}, (P_s,P_ang)=({c.Ps},{c.Pang}), Fibonacci points, "
-                            "splitmix64 densities",
-                "N": c.n, "k": c.k, "levels": c.levels, "P_s": c.Ps, "P_ang": c.Pang,
-                "parallelism": f"source-partition x{world} (Morton leaf ranges) + NCCL all-reduce" if world > 1
-                else "1 GPU",
-                "l2": "inputs larger than L2: each apply streams "
-                      f"{sum(st['segment_bytes'].values()) / 1e9:.1f} GB of cone-segment data",
-            },
+            "config": workload_config(c, world, st),
             "rel_err_vs_direct": rel_err,
             "plan_ms": plan_s * 1e3,
             "kernel_ms_per_step": kernel_ms,
