@@ -347,7 +347,7 @@ template <int PS, int PA>
 struct CousinEv {
     int64_t slot;  // segment slot (-1: none)
     int bi;        // shared-memory slot index, -1 if beyond SMAX (global fallback)
-    double gr, gi, up, Ts[PS], Tt[PA];
+    double gr, gi, us, ut, up;
 };
 
 template <int PS, int PA>
@@ -402,8 +402,8 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
             const double wr = kInv4Pi * rcp_nr(c.r);
             v.gr = cs * wr;
             v.gi = sn * wr;
-            cheb_T<PS>(c.us, v.Ts);
-            cheb_T<PA>(c.ut, v.Tt);
+            v.us = c.us;
+            v.ut = c.ut;
             v.up = c.up;
         }
         unsigned pend = __ballot_sync(~0u, v.slot >= 0);
@@ -429,8 +429,10 @@ __global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const doubl
         mbar_wait(&sbar[w][cb], (phase >> cb) & 1u);
         phase ^= 1u << cb;
         if (cur.slot >= 0) {
-            const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA>(&sbuf[w][cb][cur.bi][0], cur.Ts, cur.Tt, cur.up)
-                                          : contract_sm_lr<PS, PA>(vals + cur.slot * P, cur.Ts, cur.Tt, cur.up);
+            double Ts[PS], Tt[2] = {1.0, cur.ut};  // contract_sm_lr needs T_0, T_1 of u_theta only
+            cheb_T<PS>(cur.us, Ts);
+            const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA, false, PA>(&sbuf[w][cb][cur.bi][0], Ts, Tt, cur.up)
+                                          : contract_sm_lr<PS, PA>(vals + cur.slot * P, Ts, Tt, cur.up);
             ar = fma(cur.gr, F.x, fma(-cur.gi, F.y, ar));
             ai = fma(cur.gr, F.y, fma(cur.gi, F.x, ai));
         }
@@ -539,7 +541,7 @@ __global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams
             double Ts[PS], Tt[PA];
             cheb_T<PS>(cur.us, Ts);
             cheb_T<PA>(cur.ut, Tt);
-            const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA>(&sbuf[w][o & 1][cur.bi][0], Ts, Tt, cur.up)
+            const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA, false, PA>(&sbuf[w][o & 1][cur.bi][0], Ts, Tt, cur.up)
                                           : contract_sm_lr<PS, PA, true>(vals_d + cur.slot * P, Ts, Tt, cur.up);
             ar = fma(cur.rr, F.x, fma(-cur.ri, F.y, ar));
             ai = fma(cur.rr, F.y, fma(cur.ri, F.x, ai));

@@ -379,7 +379,7 @@ __device__ __forceinline__ double2 contract_sm(const double2* C, const double* T
 // Same contraction with a small live register set: phi innermost per (a, b)
 // (one complex accumulator), then theta, then s; 3 x 5 x 5 + 15 + 3 complex x
 // real MACs as contract_sm.  Tp is formed from u_phi by the recurrence.
-template <int PS, int PA, bool GLOBAL = false>
+template <int PS, int PA, bool GLOBAL = false, int UNR = 1>
 __device__ __forceinline__ double2 contract_sm_lr(const double2* C, const double* Ts, const double* Tt, double up) {
     // theta outermost and rolled (T_b by recurrence from Tt[0..1]); per b the
     // 3 x 5 (s, phi) slab: phi contraction, then accumulate T_b * (.) per s.
@@ -390,7 +390,7 @@ __device__ __forceinline__ double2 contract_sm_lr(const double2* C, const double
     for (int a = 0; a < PS; ++a) xr[a] = xi[a] = 0.0;
     const double ut = PA > 1 ? Tt[1] : 0.0, u2 = 2.0 * ut;
     double tbm1 = 0.0, tb = 1.0;
-#pragma unroll 1
+#pragma unroll UNR
     for (int b = 0; b < PA; ++b) {
         const double2* Cb = C + b * PS;
 #pragma unroll
