@@ -6,6 +6,7 @@
 // Every output has exactly one writer (target-major K3/K6, parent-node-major
 // K7): no atomics on values, deterministic results.
 #include <climits>
+
 #include <cstdio>
 #include <cmath>
 
@@ -351,7 +352,8 @@ struct CousinEv {
 };
 
 template <int PS, int PA>
-__global__ void __launch_bounds__(128, 4) k_cousin_ws(LevelParams L, const double* __restrict__ px,
+// 5 blocks/SM (96 registers) measured best for K6
+__global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const double* __restrict__ px,
                                                    const double* __restrict__ py, const double* __restrict__ pz,
                                                    const double2* __restrict__ vals, double k, double2* out,
                                                    int* bad, int smax) {
