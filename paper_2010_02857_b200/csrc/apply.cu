@@ -7,6 +7,7 @@
 // K7): no atomics on values, deterministic results.
 #include <climits>
 
+
 #include <cstdio>
 #include <cmath>
 
@@ -89,7 +90,7 @@ __global__ void k_unpermute(const double2* __restrict__ in, const int* __restric
 // One warp per (leaf, 32 targets).  The neighbours' sources are staged per warp
 // in shared memory in chunks of 32 (one coalesced load per lane), then every
 // lane sweeps the chunk (broadcast reads); 1/r from one rsqrt, phase by fm::sincos.
-__global__ void __launch_bounds__(TPB) k_near(LevelParams L, const double* __restrict__ px,
+__global__ void __launch_bounds__(TPB, 8) k_near(LevelParams L, const double* __restrict__ px,
                                               const double* __restrict__ py, const double* __restrict__ pz,
                                               const double2* __restrict__ a, double k, double2* out) {
     __shared__ double sx[TPB / 32][32], sy[TPB / 32][32], sz[TPB / 32][32];
@@ -170,7 +171,7 @@ __device__ __forceinline__ void node_off(const LevelParams& LP, int Ps, int Pa, 
 // K4: V[B, gamma, y] = sum_{m in B} a_m (|y-c|/|y-x_m|) e^{ik(|y-x_m| - |y-c|)}
 // (eq. factored_f P:432-434 at the nodes of eq. interp_pts), block per owned leaf.
 constexpr int S2C_CHUNK = 256;
-__global__ void __launch_bounds__(TPB) k_s2c(LevelParams L, const double* __restrict__ px,
+__global__ void __launch_bounds__(TPB, 8) k_s2c(LevelParams L, const double* __restrict__ px,
                                              const double* __restrict__ py, const double* __restrict__ pz,
                                              const double2* __restrict__ a, double k, int Ps, int Pa,
                                              double2* vals) {
