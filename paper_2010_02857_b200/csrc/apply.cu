@@ -1343,7 +1343,7 @@ struct Tc2Cfg {
     static constexpr int P = 75, KS = 19, NR = 10, NW = 80;
     static constexpr int J = kChunkTC2;
     static constexpr int UM = 8;
-    static constexpr int NT = 256;
+    static constexpr int NT = 256;  // 2 blocks/SM (measured: 192 threads 214 ms, 384 threads 280 ms, 256 200 ms at cfg4 6->5)
     static constexpr int NWARP = NT / 32;
     static constexpr int R = (NW + 31) / 32;
     static constexpr int FG = 8;  // fit group (aliases the geometry)
@@ -1366,7 +1366,7 @@ struct Tc2Cfg {
 };
 
 template <int PS, int PA>
-__global__ void __launch_bounds__(256, 2) k_upward_tc2(LevelParams L, LevelParams LP,
+__global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParams L, LevelParams LP,
                                                        const double2* __restrict__ vals_d, double k,
                                                        const double* __restrict__ Ms, const double* __restrict__ Ma,
                                                        double2* vals_p, int* bad, int umax,
@@ -1415,8 +1415,7 @@ __global__ void __launch_bounds__(256, 2) k_upward_tc2(LevelParams L, LevelParam
         sChild[t] = B;
     }
     __syncthreads();
-    {
-        const int o = warp;
+    for (int o = warp; o < 8; o += NWARP) {
         int base = 0;
         for (int j0 = 0; j0 < J; j0 += 32) {
             const int j = j0 + lane;
@@ -1462,8 +1461,7 @@ __global__ void __launch_bounds__(256, 2) k_upward_tc2(LevelParams L, LevelParam
 
     // ---- phase 2: per octant (warp): distinct child cells ascending, stable node
     // sort by cell; cell index ui owns sorted positions [pst[ui], pst[ui + 1])
-    {
-        const int o = warp;
+    for (int o = warp; o < 8; o += NWARP) {
         int uv[R];
         bool done[R];
 #pragma unroll
