@@ -532,25 +532,42 @@ __global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams
         }
         if (lane == 0) mbar_arrive_expect_tx(&sbar[w][buf], (unsigned)(nd * P * sizeof(double2)));
     };
+    // octants with a child for some lane of the warp (the others are skipped)
+    unsigned mymask = 0u;
+    if (active)
+        for (int o = 0; o < 8; ++o) {
+            const int B = LP.child_oct[8 * Q + o];
+            if (B >= L.b0 && B < L.b1) mymask |= 1u << o;
+        }
+    unsigned omask = __reduce_or_sync(~0u, mymask);
     double ar = 0.0, ai = 0.0;
     Ev cur, nxt;
-    prep(0, cur, 0);
-#pragma unroll 1
-    for (int o = 0; o < 8; ++o) {
-        if (o + 1 < 8) prep(o + 1, nxt, (o + 1) & 1);
-        mbar_wait(&sbar[w][o & 1], (phase >> (o & 1)) & 1u);
-        phase ^= 1u << (o & 1);
+    int oc = omask ? __ffs(omask) - 1 : 8;
+    if (oc < 8) {
+        omask &= omask - 1;
+        prep(oc, cur, 0);
+    }
+    for (int it = 0; oc < 8; ++it) {
+        const int on = omask ? __ffs(omask) - 1 : 8;
+        if (on < 8) {
+            omask &= omask - 1;
+            prep(on, nxt, (it + 1) & 1);
+        }
+        const int cb = it & 1;
+        mbar_wait(&sbar[w][cb], (phase >> cb) & 1u);
+        phase ^= 1u << cb;
         if (cur.slot >= 0) {
             double Ts[PS], Tt[PA];
             cheb_T<PS>(cur.us, Ts);
             cheb_T<PA>(cur.ut, Tt);
-            const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA, false, PA>(&sbuf[w][o & 1][cur.bi][0], Ts, Tt, cur.up)
+            const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA, false, PA>(&sbuf[w][cb][cur.bi][0], Ts, Tt, cur.up)
                                           : contract_sm_lr<PS, PA, true>(vals_d + cur.slot * P, Ts, Tt, cur.up);
             ar = fma(cur.rr, F.x, fma(-cur.ri, F.y, ar));
             ai = fma(cur.rr, F.y, fma(cur.ri, F.x, ai));
         }
-        __syncwarp();  // slot buffer (o & 1) is refilled by prep(o + 2)
+        __syncwarp();  // slot buffer cb is refilled two steps ahead
         cur = nxt;
+        oc = on;
     }
     if (active) vals_p[t] = make_double2(ar, ai);
 }
