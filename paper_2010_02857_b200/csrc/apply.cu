@@ -1038,7 +1038,7 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const int64_t c = blockIdx.x;
+    const int64_t c = LP.chunk_order ? LP.chunk_order[blockIdx.x] : blockIdx.x;
     const int s0 = LP.chunk_start[c];
     const int s1 = (c + 1 < LP.nchunk) ? LP.chunk_start[c + 1] : (int)LP.nseg;
     const int cnt = min(J, s1 - s0);
@@ -1410,7 +1410,7 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const int64_t c = blockIdx.x;
+    const int64_t c = LP.chunk_order ? LP.chunk_order[blockIdx.x] : blockIdx.x;
     const int s0 = LP.chunk_start[c];
     const int s1 = (c + 1 < LP.nchunk) ? LP.chunk_start[c + 1] : (int)LP.nseg;
     const int cnt = min(J, s1 - s0);

@@ -90,6 +90,7 @@ struct LevelParams {  // passed by value to kernels
     const int* cell_seg;
     const int* chunk_start;
     int64_t nchunk;
+    const int* chunk_order;  // execution order of the chunks (TC levels, L2 locality) or null
     // K7 kernel of the pass into this level (as PARENT level), chosen at plan time
     // from the segments per cell: 0 = cell-grouped staged DFMA (chunks of
     // <= kChunk), 1 = FP64 tensor-core GEMM (chunks of <= kChunkTC), 2 =
@@ -112,7 +113,7 @@ struct LevelHost {
     double *cos_tb = nullptr, *cphi = nullptr, *sphi = nullptr;
     double *rtab = nullptr, *st_tab = nullptr, *ct_tab = nullptr, *sp_tab = nullptr, *cp_tab = nullptr;
     int2* witems = nullptr;
-    int *child_oct = nullptr, *cell_seg = nullptr, *chunk_start = nullptr;
+    int *child_oct = nullptr, *cell_seg = nullptr, *chunk_start = nullptr, *chunk_order = nullptr;
     int64_t ncou = 0, nnbr = 0;
     std::vector<int> box_ijk_host;  // kept for plan export (small levels only)
 };

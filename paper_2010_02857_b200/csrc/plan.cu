@@ -343,6 +343,28 @@ __global__ void k_chunk_emit(const int* __restrict__ flag, const int* __restrict
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n && flag[i]) start[incl[i] - 1] = (int)i;
 }
+// Execution order of a level's TC chunks (L2 locality of the child coefficients):
+// key = (tile, parent cell coarsened to the child grid, chunk index within its
+// run, sub-cell), so the sibling cells that read the same child cells run their
+// k-th chunks (the same boxes) at the same time.
+__global__ void k_chunk_keys(const int* __restrict__ chunk_start, int64_t nch, const int* __restrict__ cell_seg,
+                             const int* __restrict__ seg_box, const int* __restrict__ seg_cell,
+                             const int* __restrict__ rsm, int64_t tile, int ch, int ns, int nC, int fs, int fc,
+                             int bsub, int bk, int bcoarse, uint64_t* key, int* val) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nch) return;
+    const int s = chunk_start[c];
+    const int seg = cell_seg[s];
+    const int cell = seg_cell[seg];
+    const int is = cell % ns, it = (cell / ns) % nC, ip = cell / (ns * nC);
+    const int nsc = ns / fs, ncc = nC / fc;
+    const uint64_t coarse = ((uint64_t)(ip / fc) * ncc + (it / fc)) * nsc + (is / fs);
+    const uint64_t sub = ((uint64_t)(ip % fc) * fc + (it % fc)) * fs + (is % fs);
+    const uint64_t k = (uint64_t)((s - rsm[s]) / ch);
+    const uint64_t tl = (uint64_t)(seg_box[seg] / tile);
+    key[c] = (((tl << bcoarse | coarse) << bk | k) << bsub) | sub;
+    val[c] = (int)c;
+}
 struct MaxOp {
     __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
 };
@@ -941,6 +963,40 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         L.p.cell_seg = L.cell_seg;
         L.p.chunk_start = L.chunk_start;
         L.p.nchunk = nch;
+        L.p.chunk_order = nullptr;
+        if ((kern == 1 || kern == 3) && d < D && !std::getenv("IFGF_NO_CHUNK_ORDER")) {
+            const LevelParams& LC = p->lev[d + 1].p;  // child grid
+            const int fs = std::max(1, L.p.ns / std::max(1, LC.ns)), fc = std::max(1, L.p.nC / std::max(1, LC.nC));
+            auto nbits = [](uint64_t v) { int b = 1; while (b < 63 && ((uint64_t)1 << b) <= v) ++b; return b; };
+            const int64_t tile = (int64_t)std::max(1.0, tile_bytes / std::max(1.0, child_bytes_per_box));
+            const int ch = kern == 3 ? kChunkTC2 : kChunkTC;
+            const int bsub = nbits((uint64_t)(fs * fc * fc));
+            const int bk = nbits((uint64_t)(ns / ch + 1));
+            const int bcoarse = nbits((uint64_t)(L.p.ncell / (fs * fc * fc) + 1));
+            const int btile = nbits((uint64_t)(L.p.nbox / tile + 1));
+            if (btile + bcoarse + bk + bsub <= 64) {
+                uint64_t* kin = S.get<uint64_t>(nch);
+                uint64_t* kout = S.get<uint64_t>(nch);
+                int* vin = S.get<int>(nch);
+                L.chunk_order = dev_alloc<int>(p, nch);
+                k_chunk_keys<<<nblocks(nch), TPB, 0, st>>>(L.chunk_start, nch, L.cell_seg, L.seg_box, L.seg_cell, rsm,
+                                                           tile, ch, L.p.ns, L.p.nC, fs, fc, bsub, bk, bcoarse, kin,
+                                                           vin);
+                size_t bytes = 0;
+                const int nb = btile + bcoarse + bk + bsub;
+                IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, L.chunk_order, (int)nch, 0,
+                                                          nb, st));
+                void* tmp = S.get<char>((int64_t)bytes);
+                IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, L.chunk_order, (int)nch, 0, nb,
+                                                          st));
+                IFGF_CUDA(cudaStreamSynchronize(st));
+                S.release(tmp);
+                S.release(kin);
+                S.release(kout);
+                S.release(vin);
+                L.p.chunk_order = L.chunk_order;
+            }
+        }
         S.release(vals_in);
         S.release(keys_out);
         S.release(rs);
