@@ -1174,38 +1174,40 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
     // ---- phase 4: per octant, W_o then DMMA tasks
     const int gid = lane >> 2, tig = lane & 3;
     long long t_task0 = 0;
+    // zero the basis padding (rows P..NW-1, columns P..KP-1) once; the octants
+    // only rewrite the P x P block (the first barrier below orders it)
+    for (int t = tid; t < NW * KP; t += NT) {
+        const int pos = t / KP, kk = t - pos * KP;
+        if (pos >= P || kk >= P) sW[t] = 0.0;
+    }
     for (int o = 0; o < 8; ++o) {
         const int no = sNo[o];
         if (no == 0) continue;
         const int U = sUn[o];
         const double* g0 = sG + (size_t)o * NW * 5;
         if (U <= umax) {
-            for (int t = tid; t < NW * PA; t += NT) {
+            // basis rows of the P real nodes (P * PA items: one round for NT >= 375);
+            // the padding rows and columns were zeroed once per chunk
+            for (int t = tid; t < P * PA; t += NT) {
                 const int pos = t / PA, cc = t - pos * PA;
                 double* wrow = sW + pos * KP;
-                if (pos < P) {
-                    const double* g = g0 + (int)sOrd[o * NW + pos] * 5;
-                    double Ts[PS], Tt[PA];
-                    cheb_T<PS>(g[0], Ts);
-                    cheb_T<PA>(g[1], Tt);
-                    const double up = g[2];
-                    double tm1 = 1.0, tp = up;
-                    if (cc == 0) tp = 1.0;
-                    for (int i = 2; i <= cc; ++i) {
-                        const double tn = fma(2.0 * up, tp, -tm1);
-                        tm1 = tp;
-                        tp = tn;
-                    }
+                const double* g = g0 + (int)sOrd[o * NW + pos] * 5;
+                double Ts[PS], Tt[PA];
+                cheb_T<PS>(g[0], Ts);
+                cheb_T<PA>(g[1], Tt);
+                const double up = g[2];
+                double tm1 = 1.0, tp = up;
+                if (cc == 0) tp = 1.0;
+                for (int i = 2; i <= cc; ++i) {
+                    const double tn = fma(2.0 * up, tp, -tm1);
+                    tm1 = tp;
+                    tp = tn;
+                }
 #pragma unroll
-                    for (int b = 0; b < PA; ++b) {
-                        const double tb = Tt[b] * tp;
+                for (int b = 0; b < PA; ++b) {
+                    const double tb = Tt[b] * tp;
 #pragma unroll
-                        for (int a = 0; a < PS; ++a) wrow[(cc * PA + b) * PS + a] = Ts[a] * tb;
-                    }
-                    if (cc == 0)
-                        for (int kk = P; kk < KP; ++kk) wrow[kk] = 0.0;
-                } else {
-                    for (int kk = cc; kk < KP; kk += PA) wrow[kk] = 0.0;
+                    for (int a = 0; a < PS; ++a) wrow[(cc * PA + b) * PS + a] = Ts[a] * tb;
                 }
             }
             __syncthreads();
