@@ -1044,20 +1044,35 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
     const int cnt = min(J, s1 - s0);
 
     // ---- phase 0
-    for (int j = tid; j < J; j += NT) sSeg[j] = j < cnt ? LP.cell_seg[s0 + j] : -1;
-    for (int t = tid; t < PS * PS; t += NT) sMs[t] = Ms[t];
-    for (int t = tid; t < PA * PA; t += NT) sMa[t] = Ma[t];
+    __shared__ int sBox[J];
+    for (int j = tid; j < J; j += NT) {
+        int seg = -1, box = -1;
+        if (j < cnt) {
+            seg = LP.cell_seg[s0 + j];
+            box = LP.seg_box[seg];
+        }
+        sSeg[j] = seg;
+        sBox[j] = box;
+    }
     for (int t = tid; t < J * P; t += NT) sV[t] = make_double2(0.0, 0.0);
     __syncthreads();
-    for (int t = tid; t < 8 * J; t += NT) {
-        const int o = t / J, j = t - o * J;
-        const int seg = sSeg[j];
-        int B = -1;
-        if (seg >= 0) {
-            B = LP.child_oct[8 * LP.seg_box[seg] + o];
-            if (B < L.b0 || B >= L.b1) B = -1;
+    // children by octant: the two rounds' loads are issued together
+    for (int t0 = tid; t0 < 8 * J; t0 += 2 * NT) {
+        int Bv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = t0 + h * NT;
+            Bv[h] = -1;
+            if (t < 8 * J) {
+                const int o = t / J, j = t - o * J;
+                if (sBox[j] >= 0) Bv[h] = LP.child_oct[8 * sBox[j] + o];
+            }
         }
-        sChild[t] = B;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = t0 + h * NT;
+            if (t < 8 * J) sChild[t] = (Bv[h] < L.b0 || Bv[h] >= L.b1) ? -1 : Bv[h];
+        }
     }
     __syncthreads();
     if (warp < 8) {
@@ -1154,18 +1169,45 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
     __syncthreads();
     mark(2);
 
-    // ---- phase 3: child segment slots per (octant, cell, compacted segment);
-    // -1 = no column (the B fragment then reads the zero segment)
-    for (int t = tid; t < 8 * UM * J; t += NT) {
-        const int o = t / (UM * J), rem = t - o * (UM * J), ui = rem / J, q = rem - ui * J;
-        int sl = -1;
-        if (ui < sUn[o] && sUn[o] <= umax && q < sNo[o]) {
-            const int B = sChild[o * J + sJl[o * J + q]];
-            const int64_t s64 = seg_slot(L, B, sUcell[o * UM + ui]);
-            if (s64 < 0) atomicOr(bad, 1);
-            sl = (int)s64;
+    // ---- phase 3: child segment slots of the staged (octant, cell, compacted
+    // segment) triples only (tasks treat columns q >= n_o as absent); two items
+    // per thread in flight
+    {
+        __shared__ int sPre[9];
+        if (tid == 0) {
+            int acc = 0;
+            for (int o = 0; o < 8; ++o) {
+                sPre[o] = acc;
+                if (sUn[o] <= umax) acc += sUn[o] * sNo[o];
+            }
+            sPre[8] = acc;
         }
-        sSlot[t] = sl;
+        __syncthreads();
+        const int tot = sPre[8];
+        for (int t0 = tid; t0 < tot; t0 += 2 * NT) {
+            int idx[2], Bv[2], cellv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int t = t0 + h * NT;
+                idx[h] = -1;
+                if (t < tot) {
+                    int o = 0;
+                    while (o < 7 && t >= sPre[o + 1]) ++o;
+                    const int rem = t - sPre[o], no = sNo[o];
+                    const int ui = rem / no, q = rem - ui * no;
+                    idx[h] = (o * UM + ui) * J + q;
+                    Bv[h] = sChild[o * J + sJl[o * J + q]];
+                    cellv[h] = sUcell[o * UM + ui];
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (idx[h] < 0) continue;
+                const int64_t s64 = seg_slot(L, Bv[h], cellv[h]);
+                if (s64 < 0) atomicOr(bad, 1);
+                sSlot[idx[h]] = (int)s64;
+            }
+        }
     }
     // (no barrier: the first octant's basis build below does not read the slots,
     // and its closing barrier orders them before the first DMMA task)
@@ -1241,7 +1283,8 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
                 }
             };
             auto load_b = [&](int st, int ui, double2* bb) {
-                const int sl = sSlot[(o * UM + ui) * J + st * 8 + gid];
+                const int q = st * 8 + gid;
+                const int sl = q < no ? sSlot[(o * UM + ui) * J + q] : -1;
                 const double2* cp = sl >= 0 ? vals_d + (int64_t)sl * P : zseg;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) bb[ks] = __ldg(cp + 4 * ks + tig);
