@@ -1461,19 +1461,22 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
     const int cnt = min(J, s1 - s0);
 
     // ---- phase 0: segments, children by octant, per-octant compaction
-    for (int j = tid; j < J; j += NT) sSeg[j] = j < cnt ? LP.cell_seg[s0 + j] : -1;
-    for (int t = tid; t < PS * PS; t += NT) sMs[t] = Ms[t];
-    for (int t = tid; t < PA * PA; t += NT) sMa[t] = Ma[t];
+    __shared__ int sBox[J];
+    for (int j = tid; j < J; j += NT) {
+        int seg = -1, box = -1;
+        if (j < cnt) {
+            seg = LP.cell_seg[s0 + j];
+            box = LP.seg_box[seg];
+        }
+        sSeg[j] = seg;
+        sBox[j] = box;
+    }
     for (int t = tid; t < J * P; t += NT) sV[t] = make_double2(0.0, 0.0);
     __syncthreads();
-    for (int t = tid; t < 8 * J; t += NT) {
+    for (int t = tid; t < 8 * J; t += NT) {  // 8 J = NT: one round
         const int o = t / J, j = t - o * J;
-        const int seg = sSeg[j];
-        int B = -1;
-        if (seg >= 0) {
-            B = LP.child_oct[8 * LP.seg_box[seg] + o];
-            if (B < L.b0 || B >= L.b1) B = -1;
-        }
+        int B = sBox[j] >= 0 ? LP.child_oct[8 * sBox[j] + o] : -1;
+        if (B < L.b0 || B >= L.b1) B = -1;
         sChild[t] = B;
     }
     __syncthreads();
@@ -1565,17 +1568,44 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
     }
     __syncthreads();
 
-    // ---- phase 3: child segment slots per (octant, cell, compacted segment)
-    for (int t = tid; t < 8 * UM * J; t += NT) {
-        const int o = t / (UM * J), rem = t - o * (UM * J), ui = rem / J, q = rem - ui * J;
-        int sl = -1;
-        if (ui < sUn[o] && sUn[o] <= umax && q < sNo[o]) {
-            const int B = sChild[o * J + sJl[o * J + q]];
-            const int64_t s64 = seg_slot(L, B, sUcell[o * UM + ui]);
-            if (s64 < 0) atomicOr(bad, 1);
-            sl = (int)s64;
+    // ---- phase 3: child segment slots of the staged (octant, cell, compacted
+    // segment) triples only (tasks treat columns q >= n_o as absent)
+    {
+        __shared__ int sPre[9];
+        if (tid == 0) {
+            int acc = 0;
+            for (int o = 0; o < 8; ++o) {
+                sPre[o] = acc;
+                if (sUn[o] <= umax) acc += sUn[o] * sNo[o];
+            }
+            sPre[8] = acc;
         }
-        sSlot[t] = sl;
+        __syncthreads();
+        const int tot = sPre[8];
+        for (int t0 = tid; t0 < tot; t0 += 2 * NT) {
+            int idx[2], Bv[2], cellv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int t = t0 + h * NT;
+                idx[h] = -1;
+                if (t < tot) {
+                    int o = 0;
+                    while (o < 7 && t >= sPre[o + 1]) ++o;
+                    const int rem = t - sPre[o], no = sNo[o];
+                    const int ui = rem / no, q = rem - ui * no;
+                    idx[h] = (o * UM + ui) * J + q;
+                    Bv[h] = sChild[o * J + sJl[o * J + q]];
+                    cellv[h] = sUcell[o * UM + ui];
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (idx[h] < 0) continue;
+                const int64_t s64 = seg_slot(L, Bv[h], cellv[h]);
+                if (s64 < 0) atomicOr(bad, 1);
+                sSlot[idx[h]] = (int)s64;
+            }
+        }
     }
     __syncthreads();
 
@@ -1637,7 +1667,7 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
                 }
                 // B fragments: column q = st*8 + gid
                 const int q = st * 8 + gid;
-                const int sl = sSlot[(o * UM + ui) * J + q];
+                const int sl = q < no ? sSlot[(o * UM + ui) * J + q] : -1;
                 const double2* cp = sl >= 0 ? vals_d + (int64_t)sl * P : zseg;
                 double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
                 double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
