@@ -183,8 +183,8 @@ __global__ void __launch_bounds__(TPB, 8) k_s2c(LevelParams L, const double* __r
     const int64_t s0 = L.rank[row], s1 = L.rank[row + L.W];
     const int64_t nitem = (s1 - s0) * P;
     if (nitem == 0) return;
-    const double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
-                 cz = box_centre(L, L.box_ijk[3 * B + 2], 2);
+    double cx, cy, cz;
+    box_centre3(L, B, cx, cy, cz);
     const int m0 = L.box_start[B], m1 = L.box_start[B + 1];
     for (int64_t base = 0; base < nitem; base += blockDim.x) {
         int64_t j = base + threadIdx.x;
@@ -316,8 +316,8 @@ __global__ void __launch_bounds__(TPB) k_cousin(LevelParams L, const double* __r
     for (int e = L.cou_off[T]; e < L.cou_off[T + 1]; ++e) {
         int B = L.cou_idx[e];
         if (B < L.b0 || B >= L.b1) continue;
-        double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
-               cz = box_centre(L, L.box_ijk[3 * B + 2], 2);
+        double cx, cy, cz;
+        box_centre3(L, B, cx, cy, cz);
         Cls c = classify(L, __dsub_rn(x, cx), __dsub_rn(y, cy), __dsub_rn(z, cz));
         int64_t slot = seg_slot(L, B, cell_of(L, c));
         if (slot < 0) {
@@ -395,8 +395,8 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
         const int e = e0 + step * i + half;
         const int B = e < e1 ? L.cou_idx[e] : -1;
         if (active && B >= L.b0 && B < L.b1) {
-            const double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
-                         cz = box_centre(L, L.box_ijk[3 * B + 2], 2);
+            double cx, cy, cz;
+            box_centre3(L, B, cx, cy, cz);
             const Cls c = classify(L, __dsub_rn(x, cx), __dsub_rn(y, cy), __dsub_rn(z, cz));
             v.slot = seg_slot(L, B, cell_of(L, c));
             if (v.slot < 0) atomicOr(bad, 1);

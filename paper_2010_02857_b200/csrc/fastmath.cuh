@@ -9,7 +9,8 @@
 // are branch-light polynomials:
 //   fm_atan2: octant reduction to |t| <= tan(pi/8) with ONE division, then an odd
 //             polynomial of degree 23 (near-minimax, Chebyshev-interpolated in
-//             high precision; rel. error < 5e-18 before rounding).
+//             high precision; rel. error < 5e-18 before rounding), and one fused
+//             k pi/4 +- p reconstruction; atan2_2pi maps to [0, 2 pi] directly.
 //   fm_sincos: Cody-Waite reduction by pi/2 with a 3-part constant (FMA), then
 //             degree-15 / degree-16 polynomials on |r| <= pi/4 (abs. error < 1e-17
 //             before rounding); |x| >= 2^30 falls back to libdevice sincos.
@@ -32,8 +33,6 @@ namespace fm {
 
 constexpr double kTanPi8 = 0.41421356237309503;
 constexpr double kPi4 = 0.7853981633974483, kPi4Lo = 3.061616997868383e-17;
-constexpr double kPi2 = 1.5707963267948966, kPi2Lo = 6.123233995736766e-17;
-constexpr double kPiHi = 3.141592653589793, kPiLo = 1.2246467991473532e-16;
 constexpr double k2OverPi = 0.6366197723675814;
 constexpr double kPio2_1 = 1.5707963267948966, kPio2_2 = 6.123233995736766e-17, kPio2_3 = -1.4973849048591698e-33;
 
@@ -106,10 +105,16 @@ static constexpr double kCosC_h[6] = {
 #define IFGF_FMC(name, i) name##_h[i]
 #endif
 
-// atan2(y, x) in (-pi, pi]; (x, y) != (0, 0).
-IFGF_HD double atan2(double y, double x) {
+// Shared core of atan2 / atan2_2pi: for (x, y) != (0, 0) returns p = atan(t) of the
+// reduced argument |t| <= tan(pi/8) and the octant data such that
+//   atan2(|y|, x) = k pi/4 + sg p,  k in {0, ..., 4}, sg = +-1.
+// One compare replaces fmax/fmin (no NaN handling needed); the octant fix-ups are
+// integer selects and ONE fused k pi/4 add (k * kPi4 is exact for k <= 4: the
+// significand of kPi4 ends in three zero bits), instead of three hi/lo additions.
+IFGF_HD double atan2_core(double y, double x, int* kq, bool* neg) {
     const double ax = std::fabs(x), ay = std::fabs(y);
-    const double mx = std::fmax(ax, ay), mn = std::fmin(ax, ay);
+    const bool sw = ay > ax;
+    const double mx = sw ? ay : ax, mn = sw ? ax : ay;
     const bool big = mn > kTanPi8 * mx;  // reduce via atan(t) = pi/4 + atan((t-1)/(t+1))
     const double num = big ? mn - mx : mn, den = big ? mn + mx : mx;
 #ifdef __CUDA_ARCH__
@@ -136,14 +141,45 @@ IFGF_HD double atan2(double y, double x) {
     q = std::fma(q, s, IFGF_FMC(kAtanQ, 8));
     q = std::fma(q, s, IFGF_FMC(kAtanQ, 9));
     q = std::fma(q, s, IFGF_FMC(kAtanQ, 10));
-    double r = std::fma(t * s, q, t);  // atan(mn / mx) (- pi/4 if big)
-    const double r1 = kPi4 + (r + kPi4Lo);
-    r = big ? r1 : r;
-    const double r2 = kPi2 - (r - kPi2Lo);
-    r = ay > ax ? r2 : r;
-    const double r3 = kPiHi - (r - kPiLo);
-    r = x < 0.0 ? r3 : r;
-    return std::copysign(r, y);
+    // atan(mn/mx) = big pi/4 + p; swapped: pi/2 - that; x < 0: pi - that
+    int k = big ? 1 : 0;
+    bool ng = false;
+    if (sw) {
+        k = 2 - k;
+        ng = true;
+    }
+    if (x < 0.0) {
+        k = 4 - k;
+        ng = !ng;
+    }
+    *kq = k;
+    *neg = ng;
+    return std::fma(t * s, q, t);
+}
+
+IFGF_HD double octant_sum(int k, bool neg, double p) {
+    const double kd = (double)k;
+    return std::fma(kd, kPi4, std::fma(kd, kPi4Lo, neg ? -p : p));
+}
+
+// atan2(y, x) in [-pi, pi]; (x, y) != (0, 0).
+IFGF_HD double atan2(double y, double x) {
+    int k;
+    bool ng;
+    const double p = atan2_core(y, x, &k, &ng);
+    return std::copysign(octant_sum(k, ng, p), y);
+}
+
+// atan2(y, x) mapped to [0, 2 pi] (y < 0: 2 pi - |atan2|); (x, y) != (0, 0).
+IFGF_HD double atan2_2pi(double y, double x) {
+    int k;
+    bool ng;
+    const double p = atan2_core(y, x, &k, &ng);
+    if (y < 0.0) {
+        k = 8 - k;
+        ng = !ng;
+    }
+    return octant_sum(k, ng, p);
 }
 
 // sin and cos of x (any finite x).

@@ -52,6 +52,7 @@ struct LevelParams {  // passed by value to kernels
     int64_t b0, b1;      // owned box range [b0, b1) (source partition)
     // boxes
     const int* box_ijk;       // 3 per box
+    const double* box_c;      // 4 per box: centre x0 + (ijk + 1/2) H (IEEE, as box_centre) and 0
     const int* box_start;     // nbox + 1 (sorted point ranges)
     const int* box_parent;    // nbox
     const int* child_start;   // nbox + 1 (boxes of level d + 1)
@@ -106,6 +107,7 @@ struct LevelHost {
     LevelParams p{};
     // owned device allocations
     int *box_ijk = nullptr, *box_start = nullptr, *box_parent = nullptr, *child_start = nullptr;
+    double* box_c = nullptr;
     int *nbr_off = nullptr, *nbr_idx = nullptr, *cou_off = nullptr, *cou_idx = nullptr;
     unsigned long long* bitmap = nullptr;
     unsigned* rank = nullptr;
@@ -219,8 +221,7 @@ __device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double 
     double ph = 0.0;
     int ip = 0;
     if (!(vx == 0.0 && vy == 0.0)) {
-        ph = fm::atan2(vy, vx);
-        if (ph < 0.0) ph += 2.0 * kPi;
+        ph = fm::atan2_2pi(vy, vx);
         ip = (int)(ph * L.idth);
         ip = ip < 0 ? 0 : (ip > n2 - 1 ? n2 - 1 : ip);
         for (int iter = 0; iter < 2 * n2; ++iter) {
@@ -261,6 +262,14 @@ __device__ __forceinline__ int64_t seg_slot(const LevelParams& L, int64_t b, int
 
 __device__ __forceinline__ double box_centre(const LevelParams& L, int k, int axis) {
     return __dadd_rn(L.x0[axis], __dmul_rn((double)k + 0.5, L.H));
+}
+
+// Centre of box B from the plan's table (bit-identical to box_centre).
+__device__ __forceinline__ void box_centre3(const LevelParams& L, int B, double& cx, double& cy, double& cz) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(L.box_c) + 2 * (int64_t)B);
+    cx = a.x;
+    cy = a.y;
+    cz = __ldg(L.box_c + 4 * (int64_t)B + 2);
 }
 
 // Chebyshev polynomials T_0..T_{n-1} at u (three-term recurrence).

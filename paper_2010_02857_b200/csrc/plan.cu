@@ -139,6 +139,15 @@ __global__ void k_box_ijk(const uint64_t* __restrict__ key, int64_t nb, int* ijk
     ijk[3 * b + 2] = compact3(k);
 }
 
+// Box centres x0 + (k + 1/2) H_d, IEEE-rounded exactly as box_centre (eq.
+// defboxsizesandcenters), 4 doubles per box for aligned loads.
+__global__ void k_box_c(const int* __restrict__ ijk, int64_t nb, LevelParams L, double* c) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    for (int a = 0; a < 3; ++a) c[4 * b + a] = box_centre(L, ijk[3 * b + a], a);
+    c[4 * b + 3] = 0.0;
+}
+
 // Pairwise-different points: coincident points share a leaf.
 __global__ void k_coincident(const double* __restrict__ px, const double* __restrict__ py,
                              const double* __restrict__ pz, const int* __restrict__ start, int64_t nb, int* bad) {
@@ -236,8 +245,8 @@ __global__ void k_flag_cousin_points(LevelParams L, const double* __restrict__ p
     for (int e = L.cou_off[T]; e < L.cou_off[T + 1]; ++e) {
         int B = L.cou_idx[e];
         if (B < L.b0 || B >= L.b1) continue;
-        double cx = box_centre(L, L.box_ijk[3 * B], 0), cy = box_centre(L, L.box_ijk[3 * B + 1], 1),
-               cz = box_centre(L, L.box_ijk[3 * B + 2], 2);
+        double cx, cy, cz;
+        box_centre3(L, B, cx, cy, cz);
         Cls c = classify(L, __dsub_rn(x, cx), __dsub_rn(y, cy), __dsub_rn(z, cz));
         int64_t cell = cell_of(L, c);
         if (cell < 0 || cell >= L.ncell) { atomicOr(bad, 1); continue; }
@@ -729,6 +738,8 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             LevelHost& L = p->lev[d];
             L.box_ijk = dev_alloc<int>(p, 3 * L.p.nbox);
             k_box_ijk<<<nblocks(L.p.nbox), TPB, 0, st>>>(bkey[d], L.p.nbox, L.box_ijk);
+            L.box_c = dev_alloc<double>(p, 4 * L.p.nbox);
+            k_box_c<<<nblocks(L.p.nbox), TPB, 0, st>>>(L.box_ijk, L.p.nbox, L.p, L.box_c);
             IFGF_CUDA(cudaGetLastError());
         }
     }
@@ -822,6 +833,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
     for (int d = 1; d <= D; ++d) {
         LevelHost& L = p->lev[d];
         L.p.box_ijk = L.box_ijk;
+        L.p.box_c = L.box_c;
         L.p.box_start = L.box_start;
         L.p.box_parent = L.box_parent;
         L.p.child_start = L.child_start;
@@ -951,8 +963,8 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         const int tc = kern == 1 || kern == 3;
         L.p.up_kernel = kern;
         if (std::getenv("IFGF_PLAN_VERBOSE"))
-            fprintf(stderr, "[ifgf] level %d: %lld segments, %lld cell runs, %.2f per run, tile %.0f MB, K7 kernel %d\n",
-                    d, (long long)ns, (long long)nrun, per_run, tile_bytes / 1e6, kern);
+            fprintf(stderr, "[ifgf] level %d: %lld boxes, nC %d ns %d, %lld segments, %lld cell runs, %.2f per run, tile %.0f MB, K7 kernel %d\n",
+                    d, (long long)(L.p.b1 - L.p.b0), L.p.nC, L.p.ns, (long long)ns, (long long)nrun, per_run, tile_bytes / 1e6, kern);
         k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, kern == 3 ? kChunkTC2 : (tc ? kChunkTC : kChunk), flag);
         inclusive_scan(S, flag, incl, ns, st);
         int64_t nch = d2h_one(incl + ns - 1, st);

@@ -22,7 +22,7 @@ plan = ifgf.Plan(dp, c.k, c.levels, c.Ps, c.Pang)
 torch.cuda.synchronize()
 print(name, "plan s", time.time() - t, flush=True)
 st = plan.stats()
-print({k: st[k] for k in ("nseg", "upward_evals", "upward_kernel", "plan_device_bytes")}, flush=True)
+print({k: st[k] for k in ("nseg", "upward_evals", "cousin_evals", "upward_kernel", "plan_device_bytes")}, flush=True)
 plan.profile_enable(True)
 out = plan.apply(da)
 torch.cuda.synchronize()

@@ -46,6 +46,29 @@ def test_atan2(harness):
     assert worst < 4 * 2.0 ** -53, worst
 
 
+def test_atan2_2pi(harness):
+    # phi in [0, 2 pi]: atan2 + 2 pi for y < 0 (reading R13), one rounding
+    mp.mp.dps = 50
+    rng = np.random.default_rng(3)
+    pts = list(rng.normal(size=(4000, 2)))
+    for a in [0.0, -0.0, 1.0, -1.0, 1e-300, -1e-300, 1e300, -1e300]:
+        for b in [0.0, 1.0, -1.0, 0.41421356237309503, -2.414213562373095]:
+            if a != 0.0 or b != 0.0:
+                pts.append(np.array([a, b]))
+                pts.append(np.array([b, a]))
+    out = run(harness, [f"b {float(y)!r} {float(x)!r}" for y, x in pts])
+    worst = 0.0
+    for (y, x), got in zip(pts, out):
+        ref = mp.atan2(mp.mpf(float(y)), mp.mpf(float(x)))
+        if ref < 0:
+            ref += 2 * mp.pi
+        assert 0.0 <= float(got) <= 2 * math.pi
+        err = abs(mp.mpf(got) - ref) / max(abs(ref), mp.mpf(2.0) ** -1022)
+        if ref > 1e-300:
+            worst = max(worst, float(err))
+    assert worst < 4 * 2.0 ** -53, worst
+
+
 def test_sincos(harness):
     mp.mp.dps = 50
     rng = np.random.default_rng(2)
