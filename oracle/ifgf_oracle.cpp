@@ -173,6 +173,16 @@ struct Grid {
     std::vector<double> cos_pb, sin_pb;    // cos/sin(j dphi), j = 0..2nC (phi boundaries)
 };
 
+// (c, s) rotated by q quarter turns about z: (c, s) -> (-s, c) per turn (exact).
+void quarter_turns(double c, double s, int q, double* co, double* so) {
+    switch (q & 3) {
+        case 0: *co = c; *so = s; break;
+        case 1: *co = -s; *so = c; break;
+        case 2: *co = -c; *so = -s; break;
+        default: *co = s; *so = -c; break;
+    }
+}
+
 void grid_tables(Grid& g) {
     const double eta = std::sqrt(3.0) / 3.0;  // eta = sqrt(3)/3
     g.h = std::sqrt(3.0) / 2.0 * g.H;         // h = (sqrt(3)/2) H (eq. def_eps)
@@ -182,6 +192,18 @@ void grid_tables(Grid& g) {
     for (int k = 0; k <= g.nC; ++k) g.cos_tb[k] = std::cos((double)k * PI / (double)g.nC);
     g.cos_pb.assign(2 * g.nC + 1, 0.0);
     g.sin_pb.assign(2 * g.nC + 1, 0.0);
+    if (g.nC % 2 == 0) {
+        // n_C even: exact quarter-turn symmetry of the boundary rays (reading R18):
+        // phi_j = q pi/2 + phi_jr with jr < n_C/2; (cos, sin) of phi_jr from libm,
+        // rotated by q quarter turns ((c, s) -> (-s, c)), which is exact.
+        const int hq = g.nC / 2;
+        for (int j = 0; j <= 2 * g.nC; ++j) {
+            const int q = (j / hq) & 3, jr = j % hq;
+            const double a = (double)jr * PI / (double)g.nC;
+            quarter_turns(std::cos(a), std::sin(a), q, &g.cos_pb[j], &g.sin_pb[j]);
+        }
+        return;
+    }
     for (int j = 0; j < g.nC; ++j) {
         double a = (double)j * PI / (double)g.nC;
         g.cos_pb[j] = std::cos(a);
@@ -289,9 +311,17 @@ void node_offset(const oracle_plan& p, const Grid& g, int is, int ith, int iph, 
                  double off[3], double* r_out) {
     double s = ((double)is + (1.0 + p.ts[ks]) / 2.0) * g.ds;
     double th = ((double)ith + (1.0 + p.ta[it]) / 2.0) * g.dth;
-    double ph = ((double)iph + (1.0 + p.ta[jp]) / 2.0) * g.dth;
     double r = g.h / s;
-    double st = std::sin(th), ct = std::cos(th), sp = std::sin(ph), cp = std::cos(ph);
+    double st = std::sin(th), ct = std::cos(th), sp, cp;
+    if (g.nC % 2 == 0) {  // quarter-turn reduction of the phi sector (reading R18)
+        const int hq = g.nC / 2;
+        const double ph = ((double)(iph % hq) + (1.0 + p.ta[jp]) / 2.0) * g.dth;
+        quarter_turns(std::cos(ph), std::sin(ph), iph / hq, &cp, &sp);
+    } else {
+        const double ph = ((double)iph + (1.0 + p.ta[jp]) / 2.0) * g.dth;
+        sp = std::sin(ph);
+        cp = std::cos(ph);
+    }
     off[0] = r * st * cp;
     off[1] = r * st * sp;
     off[2] = r * ct;

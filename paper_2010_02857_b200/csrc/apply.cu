@@ -1045,14 +1045,17 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
 
     // ---- phase 0
     __shared__ int sBox[J];
+    __shared__ unsigned char sQd[J];  // quarter turns of segment j's cell from the representative
     for (int j = tid; j < J; j += NT) {
-        int seg = -1, box = -1;
+        int seg = -1, box = -1, qd = 0;
         if (j < cnt) {
             seg = LP.cell_seg[s0 + j];
             box = LP.seg_box[seg];
+            qd = sym_quarter(LP, LP.seg_cell[seg]);
         }
         sSeg[j] = seg;
         sBox[j] = box;
+        sQd[j] = (unsigned char)qd;
     }
     for (int t = tid; t < J * P; t += NT) sV[t] = make_double2(0.0, 0.0);
     __syncthreads();
@@ -1065,7 +1068,7 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
             Bv[h] = -1;
             if (t < 8 * J) {
                 const int o = t / J, j = t - o * J;
-                if (sBox[j] >= 0) Bv[h] = LP.child_oct[8 * sBox[j] + o];
+                if (sBox[j] >= 0) Bv[h] = LP.child_oct[8 * sBox[j] + rot_oct(o, sQd[j])];
             }
         }
 #pragma unroll
@@ -1091,7 +1094,7 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
     mark(0);
 
     // ---- phase 1: geometry of (octant, node)
-    const int cellp = LP.seg_cell[sSeg[0]];
+    const int cellp = sym_rep(LP, LP.seg_cell[sSeg[0]]);  // the chunk's (representative) parent cell
     const double hh = 0.5 * L.H;
     for (int t = tid; t < 8 * NW; t += NT) {
         const int o = t / NW, n = t - o * NW;
@@ -1101,8 +1104,10 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
             node_off(LP, PS, PA, cellp, n, off);
             const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
             const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
-            const Cls cl = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+            const double vx = __dadd_rn(off[0], dx), vy = __dadd_rn(off[1], dy);
+            const Cls cl = classify(L, vx, vy, __dadd_rn(off[2], dz));
             u = (int)cell_of(L, cl);
+            if (LP.sym && vx == 0.0 && vy == 0.0) u |= kPoleFlag;  // pole: sector 0 in every rotation
             // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
             const double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
             const double ic = rcp_nr(cl.r * (cl.r + rQ));
@@ -1196,8 +1201,9 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
                     const int rem = t - sPre[o], no = sNo[o];
                     const int ui = rem / no, q = rem - ui * no;
                     idx[h] = (o * UM + ui) * J + q;
-                    Bv[h] = sChild[o * J + sJl[o * J + q]];
-                    cellv[h] = sUcell[o * UM + ui];
+                    const int j = sJl[o * J + q];
+                    Bv[h] = sChild[o * J + j];
+                    cellv[h] = sym_cell(L, sUcell[o * UM + ui], sQd[j]);
                 }
             }
 #pragma unroll
@@ -1364,7 +1370,7 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
                 const int j = sJl[o * J + q];
                 const int B = sChild[o * J + j];
                 const double* g = g0 + n * 5;
-                const int64_t sl = seg_slot(L, B, sU[o * NW + n]);
+                const int64_t sl = seg_slot(L, B, sym_cell(L, sU[o * NW + n], sQd[j]));
                 if (sl < 0) {
                     atomicOr(bad, 1);
                     continue;
@@ -1462,20 +1468,23 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
 
     // ---- phase 0: segments, children by octant, per-octant compaction
     __shared__ int sBox[J];
+    __shared__ unsigned char sQd[J];  // quarter turns of segment j's cell from the representative
     for (int j = tid; j < J; j += NT) {
-        int seg = -1, box = -1;
+        int seg = -1, box = -1, qd = 0;
         if (j < cnt) {
             seg = LP.cell_seg[s0 + j];
             box = LP.seg_box[seg];
+            qd = sym_quarter(LP, LP.seg_cell[seg]);
         }
         sSeg[j] = seg;
         sBox[j] = box;
+        sQd[j] = (unsigned char)qd;
     }
     for (int t = tid; t < J * P; t += NT) sV[t] = make_double2(0.0, 0.0);
     __syncthreads();
     for (int t = tid; t < 8 * J; t += NT) {  // 8 J = NT: one round
         const int o = t / J, j = t - o * J;
-        int B = sBox[j] >= 0 ? LP.child_oct[8 * sBox[j] + o] : -1;
+        int B = sBox[j] >= 0 ? LP.child_oct[8 * sBox[j] + rot_oct(o, sQd[j])] : -1;
         if (B < L.b0 || B >= L.b1) B = -1;
         sChild[t] = B;
     }
@@ -1494,7 +1503,7 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
     __syncthreads();
 
     // ---- phase 1: geometry of (octant, node)
-    const int cellp = LP.seg_cell[sSeg[0]];
+    const int cellp = sym_rep(LP, LP.seg_cell[sSeg[0]]);  // the chunk's (representative) parent cell
     const double hh = 0.5 * L.H;
     for (int t = tid; t < 8 * NW; t += NT) {
         const int o = t / NW, n = t - o * NW;
@@ -1504,8 +1513,10 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
             node_off(LP, PS, PA, cellp, n, off);
             const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
             const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
-            const Cls cl = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+            const double vx = __dadd_rn(off[0], dx), vy = __dadd_rn(off[1], dy);
+            const Cls cl = classify(L, vx, vy, __dadd_rn(off[2], dz));
             u = (int)cell_of(L, cl);
+            if (LP.sym && vx == 0.0 && vy == 0.0) u |= kPoleFlag;  // pole: sector 0 in every rotation
             // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
             const double num = fma(dx, dx, fma(dy, dy, dz * dz)) + 2.0 * fma(off[0], dx, fma(off[1], dy, off[2] * dz));
             const double ic = rcp_nr(cl.r * (cl.r + rQ));
@@ -1594,8 +1605,9 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
                     const int rem = t - sPre[o], no = sNo[o];
                     const int ui = rem / no, q = rem - ui * no;
                     idx[h] = (o * UM + ui) * J + q;
-                    Bv[h] = sChild[o * J + sJl[o * J + q]];
-                    cellv[h] = sUcell[o * UM + ui];
+                    const int j = sJl[o * J + q];
+                    Bv[h] = sChild[o * J + j];
+                    cellv[h] = sym_cell(L, sUcell[o * UM + ui], sQd[j]);
                 }
             }
 #pragma unroll
@@ -1719,7 +1731,7 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
                 const int j = sJl[o * J + q];
                 const int B = sChild[o * J + j];
                 const double* g = g0 + n * 5;
-                const int64_t sl = seg_slot(L, B, sU[o * NW + n]);
+                const int64_t sl = seg_slot(L, B, sym_cell(L, sU[o * NW + n], sQd[j]));
                 if (sl < 0) {
                     atomicOr(bad, 1);
                     continue;

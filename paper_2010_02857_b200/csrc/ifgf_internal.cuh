@@ -97,6 +97,7 @@ struct LevelParams {  // passed by value to kernels
     // <= kChunk), 1 = FP64 tensor-core GEMM (chunks of <= kChunkTC), 2 =
     // per-evaluation geometry (no chunks, separate K5 fit)
     int up_kernel;
+    int sym;  // K7 chunks grouped by quarter-turn orbits of the parent cell (reading R18)
 };
 
 constexpr int kChunk = 16;
@@ -159,6 +160,7 @@ struct ifgf_plan_s {
     std::vector<PendingEv> pending;
     int* dev_bad = nullptr;  // device flag: apply-time invariant violation (EINTERNAL)
     int legacy_upward = 0;   // env IFGF_LEGACY_UPWARD: K7 variant override (A/B testing, tests)
+    int no_symmetry = 0;     // env IFGF_NO_SYMMETRY: K7 chunks by cell only (A/B testing, tests)
     int tc_umax = 1 << 30;
     int stage_slots = 1 << 30;  // env IFGF_STAGE_SLOTS: cap on staged child segments per warp in K6 / K7-pe (tests)
     int legacy_cousin = 0;   // env IFGF_LEGACY_COUSIN=1: per-lane global-load K6 (A/B testing)
@@ -262,6 +264,37 @@ __device__ __forceinline__ int64_t seg_slot(const LevelParams& L, int64_t b, int
 
 __device__ __forceinline__ double box_centre(const LevelParams& L, int k, int axis) {
     return __dadd_rn(L.x0[axis], __dmul_rn((double)k + 0.5, L.H));
+}
+
+// ---- quarter-turn symmetry about z (reading R18) ----------------
+// With n_C even on both levels the phi tables are exactly quarter-turn symmetric,
+// so rotating a parent cell by q quarter turns (phi sector + q n_C/2) rotates its
+// nodes exactly; the node's child-relative geometry is that of the
+// representative cell for child octant rot_oct(o, q) and child cell
+// rot_cell(u, q) (poles v_x = v_y = 0 excepted: sector 0 stays 0).
+constexpr int kPoleFlag = 1 << 30;
+__device__ __forceinline__ int rot_oct(int o, int q) {  // (x, y) -> (-y, x), q times
+    for (int i = 0; i < (q & 3); ++i) o = ((~o & 2) << 1) | ((o & 4) >> 1) | (o & 1);
+    return o;
+}
+__device__ __forceinline__ int rot_cell(const LevelParams& L, int cell, int q) {
+    const int nsc = L.ns * L.nC;
+    const int ip = cell / nsc;
+    return ((ip + q * (L.nC >> 1)) % (2 * L.nC)) * nsc + (cell - ip * nsc);
+}
+// child cell of a staged geometry entry u for a segment q quarter turns away
+__device__ __forceinline__ int sym_cell(const LevelParams& L, int u, int q) {
+    return (u & kPoleFlag) ? (u & ~kPoleFlag) : (q ? rot_cell(L, u, q) : u);
+}
+// quarter turns of parent cell `cell` and its representative (sector mod n_C/2)
+__device__ __forceinline__ int sym_quarter(const LevelParams& LP, int cell) {
+    return LP.sym ? (cell / (LP.ns * LP.nC)) / (LP.nC >> 1) : 0;
+}
+__device__ __forceinline__ int sym_rep(const LevelParams& LP, int cell) {
+    if (!LP.sym) return cell;
+    const int nsc = LP.ns * LP.nC;
+    const int ip = cell / nsc;
+    return (ip % (LP.nC >> 1)) * nsc + (cell - ip * nsc);
 }
 
 // Centre of box B from the plan's table (bit-identical to box_centre).

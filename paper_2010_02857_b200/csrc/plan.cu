@@ -335,10 +335,18 @@ __global__ void k_iota(int64_t n, int* v) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) v[i] = (int)i;
 }
+// key = (tile, cell) or, with the quarter-turn symmetry (hq = n_C/2 > 0), (tile,
+// representative cell: phi sector mod n_C/2)
 __global__ void k_tile_keys(const int* __restrict__ seg_box, const int* __restrict__ seg_cell, int64_t n,
-                            int64_t tile, int bits, uint64_t* key) {
+                            int64_t tile, int bits, int hq, int nsc, uint64_t* key) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) key[i] = ((uint64_t)(seg_box[i] / tile) << bits) | (uint64_t)seg_cell[i];
+    if (i >= n) return;
+    int cell = seg_cell[i];
+    if (hq > 0) {
+        const int ip = cell / nsc;
+        cell = (ip % hq) * nsc + (cell - ip * nsc);
+    }
+    key[i] = ((uint64_t)(seg_box[i] / tile) << bits) | (uint64_t)cell;
 }
 __global__ void k_run_start(const uint64_t* __restrict__ key, int64_t n, int* rs) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -627,15 +635,34 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         if (L.ncell > (int64_t)1 << 31) throw Error{IFGF_ENOMEM, "cone grid too fine for the cell index"};
         std::vector<double> ctb(L.nC + 1), cph(2 * L.nC + 1), sph(2 * L.nC + 1);
         for (int kk = 0; kk <= L.nC; ++kk) ctb[kk] = std::cos((double)kk * kPi / (double)L.nC);
-        for (int j = 0; j < L.nC; ++j) {
-            double a = (double)j * kPi / (double)L.nC;
-            cph[j] = std::cos(a);
-            sph[j] = std::sin(a);
-            cph[j + L.nC] = -cph[j];
-            sph[j + L.nC] = -sph[j];
+        // phi tables: n_C even -> exact quarter-turn symmetry (reading R18; the K7
+        // tensor-core kernels share one geometry between the four rotated cells);
+        // else exact half-turn symmetry
+        const int hq = L.nC / 2;
+        auto turns = [](double c, double sn, int q, double* co, double* so) {
+            switch (q & 3) {
+                case 0: *co = c; *so = sn; break;
+                case 1: *co = -sn; *so = c; break;
+                case 2: *co = -c; *so = -sn; break;
+                default: *co = sn; *so = -c; break;
+            }
+        };
+        if (L.nC % 2 == 0) {
+            for (int j = 0; j <= 2 * L.nC; ++j) {
+                const double a = (double)(j % hq) * kPi / (double)L.nC;
+                turns(std::cos(a), std::sin(a), j / hq, &cph[j], &sph[j]);
+            }
+        } else {
+            for (int j = 0; j < L.nC; ++j) {
+                double a = (double)j * kPi / (double)L.nC;
+                cph[j] = std::cos(a);
+                sph[j] = std::sin(a);
+                cph[j + L.nC] = -cph[j];
+                sph[j + L.nC] = -sph[j];
+            }
+            cph[2 * L.nC] = cph[0];
+            sph[2 * L.nC] = sph[0];
         }
-        cph[2 * L.nC] = cph[0];
-        sph[2 * L.nC] = sph[0];
         std::vector<double> rt(L.ns * Ps), stt(L.nC * Pa), ctt(L.nC * Pa), spt(2 * L.nC * Pa), cpt(2 * L.nC * Pa);
         for (int is = 0; is < L.ns; ++is)
             for (int ks = 0; ks < Ps; ++ks) {
@@ -650,9 +677,14 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             }
         for (int ip = 0; ip < 2 * L.nC; ++ip)
             for (int kp = 0; kp < Pa; ++kp) {
-                double ph = ((double)ip + (1.0 + ta[kp]) / 2.0) * L.dth;
-                spt[ip * Pa + kp] = std::sin(ph);
-                cpt[ip * Pa + kp] = std::cos(ph);
+                if (L.nC % 2 == 0) {
+                    const double ph = ((double)(ip % hq) + (1.0 + ta[kp]) / 2.0) * L.dth;
+                    turns(std::cos(ph), std::sin(ph), ip / hq, &cpt[ip * Pa + kp], &spt[ip * Pa + kp]);
+                } else {
+                    double ph = ((double)ip + (1.0 + ta[kp]) / 2.0) * L.dth;
+                    spt[ip * Pa + kp] = std::sin(ph);
+                    cpt[ip * Pa + kp] = std::cos(ph);
+                }
             }
         L.cos_tb = LH.cos_tb = upload(p, ctb, st);
         L.cphi = LH.cphi = upload(p, cph, st);
@@ -919,11 +951,18 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         int* rsm = S.get<int>(ns);
         int* incl = S.get<int>(ns);
         int* flag = rs;  // reused after the run-start max-scan
+        // Quarter-turn symmetry (reading R18): with n_C even on both levels, the four
+        // parent cells related by quarter turns about z share one child-relative
+        // geometry, so the tensor-core kernels group segments by orbit (4x longer runs).
+        const LevelParams& LCh = p->lev[d + 1].p;
+        const bool sym_ok = !p->no_symmetry && L.p.nC % 2 == 0 && LCh.nC % 2 == 0 && LCh.ncell < ((int64_t)1 << 30);
+        int sym = sym_ok ? 1 : 0;
         auto group = [&](double tb) -> int64_t {  // sort by (tile, cell, segment); number of runs
             const int64_t tile = (int64_t)std::max(1.0, tb / std::max(1.0, child_bytes_per_box));
             int tbits = 1;
             while (tbits < 32 && ((int64_t)1 << tbits) <= L.p.nbox / tile + 1) ++tbits;
-            k_tile_keys<<<nblocks(ns), TPB, 0, st>>>(L.seg_box, L.seg_cell, ns, tile, bits, keys_in);
+            k_tile_keys<<<nblocks(ns), TPB, 0, st>>>(L.seg_box, L.seg_cell, ns, tile, bits, sym ? L.p.nC / 2 : 0,
+                                                     L.p.ns * L.p.nC, keys_in);
             size_t bytes = 0;
             IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, keys_out, vals_in, L.cell_seg, (int)ns,
                                                       0, bits + tbits, st));
@@ -941,30 +980,48 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             inclusive_scan(S, flag, incl, ns, st);
             return d2h_one(incl + ns - 1, st);
         };
-        int64_t nrun = group(tile_bytes);
-        double per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
-        if (!tile_env && per_run > 1024.0) {
-            tile_bytes = std::max(32.0e6, tile_bytes * 256.0 / per_run);
+        // K7 kernel by mean segments per cell (or orbit) run (measured on B200, DESIGN.md
+        // §7): >= 24 -> FP64 tensor-core GEMM (96-chunks, basis in shared memory);
+        // 10-24 -> register-basis tensor-core GEMM (32-chunks, 2 blocks/SM) for (3, 5),
+        // else the cell-grouped staged DFMA kernel; < 10 -> per-evaluation geometry
+        // (cfg4 parent level 4, 6.5 segments per orbit run: TC2 228 ms, pe 168 ms)
+        auto choose = [&](double pr) {
+            int kn = pr >= 24.0 ? 1 : (pr >= 10.0 ? ((Ps == 3 && Pa == 5) ? 3 : 0) : 2);
+            if (p->legacy_upward == 1 || p->legacy_upward == 7) kn = 2;  // per-evaluation (1: per-lane loads)
+            if (p->legacy_upward == 3) kn = 0;                           // staged DFMA everywhere
+            if (p->legacy_upward == 5) kn = 1;                           // force the tensor-core kernel
+            if (p->legacy_upward == 8) kn = 3;                           // force the tensor-core kernel v2
+            if (P > 80 && kn == 1) kn = 0;  // TC kernel shared memory is sized for P <= 80 ((P_s, P_ang) = (3, 5))
+            if (kn == 3 && !(Ps == 3 && Pa == 5)) kn = 1;  // TC v2 k-permutation is specific to (3, 5)
+            return kn;
+        };
+        int64_t nrun = 0;
+        double per_run = 0.0;
+        auto regroup = [&]() {
             nrun = group(tile_bytes);
             per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
+            if (!tile_env && per_run > 1024.0) {
+                tile_bytes = std::max(32.0e6, tile_bytes * 256.0 / per_run);
+                nrun = group(tile_bytes);
+                per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
+            }
+        };
+        regroup();
+        int kern = choose(per_run);
+        if (sym && !(kern == 1 || kern == 3)) {  // only the tensor-core kernels use orbits
+            sym = 0;
+            tile_bytes = tile_env ? std::atof(tile_env) * 1.0e6 : 4096.0e6;
+            regroup();
+            kern = choose(per_run);
         }
         S.release(keys_in);
-        // K7 kernel by mean segments per cell run (measured on B200):
-        // many -> FP64 tensor-core GEMM (64-chunks, basis in shared memory); some ->
-        // register-basis tensor-core GEMM (32-chunks, 2 blocks/SM) for (3, 5), else the
-        // cell-grouped staged DFMA kernel; ~1-2 -> per-evaluation geometry
-        int kern = per_run >= 24.0 ? 1 : (per_run >= 6.0 ? ((Ps == 3 && Pa == 5) ? 3 : 0) : 2);
-        if (p->legacy_upward == 1 || p->legacy_upward == 7) kern = 2;  // per-evaluation (1: per-lane loads)
-        if (p->legacy_upward == 3) kern = 0;                           // staged DFMA everywhere
-        if (p->legacy_upward == 5) kern = 1;                           // force the tensor-core kernel
-        if (p->legacy_upward == 8) kern = 3;                           // force the tensor-core kernel v2
-        if (P > 80 && kern == 1) kern = 0;  // TC kernel shared memory is sized for P <= 80 ((P_s, P_ang) = (3, 5))
-        if (kern == 3 && !(Ps == 3 && Pa == 5)) kern = 1;  // TC v2 k-permutation is specific to (3, 5)
         const int tc = kern == 1 || kern == 3;
         L.p.up_kernel = kern;
+        L.p.sym = sym;
         if (std::getenv("IFGF_PLAN_VERBOSE"))
-            fprintf(stderr, "[ifgf] level %d: %lld boxes, nC %d ns %d, %lld segments, %lld cell runs, %.2f per run, tile %.0f MB, K7 kernel %d\n",
-                    d, (long long)(L.p.b1 - L.p.b0), L.p.nC, L.p.ns, (long long)ns, (long long)nrun, per_run, tile_bytes / 1e6, kern);
+            fprintf(stderr, "[ifgf] level %d: %lld boxes, nC %d ns %d, %lld segments, %lld %s runs, %.2f per run, tile %.0f MB, K7 kernel %d\n",
+                    d, (long long)(L.p.b1 - L.p.b0), L.p.nC, L.p.ns, (long long)ns, (long long)nrun,
+                    sym ? "orbit" : "cell", per_run, tile_bytes / 1e6, kern);
         k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, kern == 3 ? kChunkTC2 : (tc ? kChunkTC : kChunk), flag);
         inclusive_scan(S, flag, incl, ns, st);
         int64_t nch = d2h_one(incl + ns - 1, st);

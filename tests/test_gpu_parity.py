@@ -223,18 +223,45 @@ def test_cousin_kernel_variants(ifgf, legacy, slots, monkeypatch):
     assert oracle.rel_l2(got, ref) <= PARITY
 
 
-def test_default_kernel_choice_tc_and_staged(ifgf):
+@pytest.mark.parametrize("nosym", ["0", "1"])
+def test_default_kernel_choice_tc_and_staged(ifgf, nosym, monkeypatch):
     """At the default settings a lambda/4-leaf sphere uses the FP64 tensor-core
-    K7 on its fine levels and the staged DFMA K7 on the coarse ones; both match
-    the oracle."""
+    K7 on its fine levels and a per-evaluation or staged K7 on the coarse ones;
+    all match the oracle, with and without the quarter-turn orbit grouping
+    (reading R18; IFGF_NO_SYMMETRY=1: cells only), and both groupings give the
+    same field up to rounding."""
+    monkeypatch.setenv("IFGF_NO_SYMMETRY", nosym)
     n, k, D = 60000, 8 * math.pi, 6
     pts = inputs.fibonacci_sphere(n)
     a = inputs.densities(n, seed=5)
     _, got, st = run_gpu(ifgf, pts, a, k, D)
     kern = st["upward_kernel"]
-    assert kern[D] == 1 and kern[4] in (0, 2, 3), kern
+    assert kern[D] == 1 and all(kern[d] in (0, 1, 2, 3) for d in range(4, D + 1)), kern
     ref = oracle.OraclePlan(pts, k, D, 3, 5).apply(a)
     assert oracle.rel_l2(got, ref) <= PARITY
+
+
+@pytest.mark.parametrize("mode,umax,leaf_nc", [("5", None, 2), ("8", None, 2), ("5", "0", 2), ("5", None, 3),
+                                               ("8", None, 3)])
+def test_symmetry_orbit_grouping(ifgf, mode, umax, leaf_nc, monkeypatch):
+    """K7 tensor-core kernels with segments grouped by quarter-turn orbits (one
+    geometry for the four rotated parent cells, rotated child octants and cells)
+    against the oracle and against the cell-only grouping.  leaf_nc = 3 makes the
+    finest level's n_C odd (orbits disabled there, enabled above); umax = 0 sends
+    every octant through the per-(segment, node) fallback."""
+    monkeypatch.setenv("IFGF_LEGACY_UPWARD", mode)
+    if umax is not None:
+        monkeypatch.setenv("IFGF_TC_UMAX", umax)
+    n, k, D = 20000, 6 * math.pi, 5
+    pts = inputs.rough_sphere(n)
+    a = inputs.densities(n, seed=11)
+    monkeypatch.setenv("IFGF_NO_SYMMETRY", "0")
+    _, got, _ = run_gpu(ifgf, pts, a, k, D, leaf_nc=leaf_nc)
+    monkeypatch.setenv("IFGF_NO_SYMMETRY", "1")
+    _, plain, _ = run_gpu(ifgf, pts, a, k, D, leaf_nc=leaf_nc)
+    ref = oracle.OraclePlan(pts, k, D, 3, 5, leaf_nc=leaf_nc).apply(a)
+    assert oracle.rel_l2(got, ref) <= PARITY
+    assert oracle.rel_l2(got, plain) <= PARITY
 
 
 # ------------------------------------------------------------ larger configs
