@@ -1091,6 +1091,7 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
         if (lane == 0) sNo[o] = base;
     }
     __syncthreads();
+    if (phase_clk && tid == 0) atomicAdd(phase_clk + 13, 1ull);
     mark(0);
 
     // ---- phase 1: geometry of (octant, node)
@@ -1271,6 +1272,12 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
             int S = 0;
             for (int u = 0; u < U; ++u) S += ((pst[u + 1] - 1) >> 3) - (pst[u] >> 3) + 1;
             const int T = nst * S;
+            if (phase_clk && tid == 0) {  // shape counters: cells, node tiles, segments, octants
+                atomicAdd(phase_clk + 9, (unsigned long long)U);
+                atomicAdd(phase_clk + 10, (unsigned long long)S);
+                atomicAdd(phase_clk + 11, (unsigned long long)no);
+                atomicAdd(phase_clk + 12, 1ull);
+            }
             const int tau0 = (int)((int64_t)warp * T / NWARP), tau1 = (int)((int64_t)(warp + 1) * T / NWARP);
             // decode task tau -> (st, ui, first tile of ui, tiles left in the group)
             auto decode = [&](int tau, int& st, int& ui, int& tl0, int& off) {
@@ -1909,6 +1916,23 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
             });
         pr.done();
     };
+    auto phase_dump = [&](int dl) {
+        if (!p->phase_clk) return;
+        unsigned long long h[16];
+        IFGF_CUDA(cudaMemcpyAsync(h, p->phase_clk, sizeof(h), cudaMemcpyDeviceToHost, st));
+        IFGF_CUDA(cudaStreamSynchronize(st));
+        IFGF_CUDA(cudaMemsetAsync(p->phase_clk, 0, sizeof(h), st));
+        double tot = 0;
+        for (int i = 0; i < 7; ++i) tot += (double)h[i];
+        fprintf(stderr, "[ifgf] level %d TC K7 phase clocks (block-thread-0 sums, %% of total %.3g):", dl, tot);
+        for (int i = 0; i < 7; ++i) fprintf(stderr, " p%d=%.1f%%", i, 100.0 * (double)h[i] / (tot > 0 ? tot : 1));
+        fprintf(stderr, "; task-loop warp utilisation %.1f%% (%d warps); per octant: %.2f cells, %.2f node tiles, "
+                "%.1f segments; %.2f octants per chunk\n",
+                100.0 * (double)h[8] / ((double)TcCfg<3, 5>::NWARP * (double)(h[5] > 0 ? h[5] : 1)),
+                TcCfg<3, 5>::NWARP, (double)h[9] / std::max(1.0, (double)h[12]),
+                (double)h[10] / std::max(1.0, (double)h[12]), (double)h[11] / std::max(1.0, (double)h[12]),
+                (double)h[12] / std::max(1.0, (double)h[13]));
+    };
     if (have) fit(D);
     for (int d = D; d >= 3 && have; --d) {
         LevelParams& L = p->lev[d].p;
@@ -1934,24 +1958,12 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
                     [&] { fused = Kern<5, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
                     [&] { fused = Kern<0, 0>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); });
                 pr.done();
+                phase_dump(d - 1);
                 if (!fused) fit(d - 1);
             }
         } else {
             have = false;
         }
-    }
-    if (p->phase_clk) {
-        unsigned long long h[16];
-        IFGF_CUDA(cudaMemcpyAsync(h, p->phase_clk, sizeof(h), cudaMemcpyDeviceToHost, st));
-        IFGF_CUDA(cudaStreamSynchronize(st));
-        IFGF_CUDA(cudaMemsetAsync(p->phase_clk, 0, sizeof(h), st));
-        double tot = 0;
-        for (int i = 0; i < 7; ++i) tot += (double)h[i];
-        fprintf(stderr, "[ifgf] TC K7 phase clocks (block-thread-0 sums, %% of total %.3g):", tot);
-        for (int i = 0; i < 7; ++i) fprintf(stderr, " p%d=%.1f%%", i, 100.0 * (double)h[i] / (tot > 0 ? tot : 1));
-        fprintf(stderr, "; task-loop warp utilisation %.1f%% (%d warps)\n",
-                100.0 * (double)h[8] / ((double)TcCfg<3, 5>::NWARP * (double)(h[5] > 0 ? h[5] : 1)),
-                TcCfg<3, 5>::NWARP);
     }
     {
         Prof pr(p, st, 6);

@@ -235,6 +235,7 @@ ifgf_status ifgf_plan(const double* points, int64_t n, double k, int levels, int
     p->P = P_s * P_ang * P_ang;
     if (const char* e = std::getenv("IFGF_LEGACY_UPWARD")) p->legacy_upward = std::atoi(e);
     if (const char* e = std::getenv("IFGF_NO_SYMMETRY")) p->no_symmetry = std::atoi(e);
+    if (const char* e = std::getenv("IFGF_EXACT_CLASSIFY")) p->cls_exact = std::atoi(e);
     if (const char* e = std::getenv("IFGF_TC_UMAX")) p->tc_umax = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("IFGF_STAGE_SLOTS")) p->stage_slots = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("IFGF_LEGACY_COUSIN")) p->legacy_cousin = std::atoi(e);

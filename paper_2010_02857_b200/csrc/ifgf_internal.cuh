@@ -98,6 +98,7 @@ struct LevelParams {  // passed by value to kernels
     // per-evaluation geometry (no chunks, separate K5 fit)
     int up_kernel;
     int sym;  // K7 chunks grouped by quarter-turn orbits of the parent cell (reading R18)
+    int cls_exact;  // 1: classify always takes the exact IEEE chain (env IFGF_EXACT_CLASSIFY; tests)
 };
 
 constexpr int kChunk = 16;
@@ -161,6 +162,7 @@ struct ifgf_plan_s {
     int* dev_bad = nullptr;  // device flag: apply-time invariant violation (EINTERNAL)
     int legacy_upward = 0;   // env IFGF_LEGACY_UPWARD: K7 variant override (A/B testing, tests)
     int no_symmetry = 0;     // env IFGF_NO_SYMMETRY: K7 chunks by cell only (A/B testing, tests)
+    int cls_exact = 0;       // env IFGF_EXACT_CLASSIFY: no classification fast path (tests)
     int tc_umax = 1 << 30;
     int stage_slots = 1 << 30;  // env IFGF_STAGE_SLOTS: cap on staged child segments per warp in K6 / K7-pe (tests)
     int legacy_cousin = 0;   // env IFGF_LEGACY_COUSIN=1: per-lane global-load K6 (A/B testing)
@@ -196,27 +198,55 @@ struct Cls {
 
 // Classification of the relative vector v at a level (DESIGN.md
 // "Classification contract", reading R7).  The
-// discrete decisions use only IEEE-rounded + - * / sqrt without contraction
-// (explicit __d*_rn) against host-libm boundary tables: r, s = h/r,
-// i_s = floor(s/ds), cos(theta) = v_z/r and the phi cross products.  The
-// angles theta = atan2(rho, v_z), phi = atan2(v_y, v_x) (reading R13) come from
-// the lean fm::atan2 and only supply the first guesses (corrected by the exact
-// comparisons) and the local coordinates u = 2 (v - v_a)/dv - 1 (values).
+// discrete decisions are those of IEEE-rounded + - * / sqrt without contraction
+// against host-libm boundary tables: r, s = h/r, i_s = floor(s/ds),
+// cos(theta) = v_z/r and the phi cross products.  The angles
+// theta = atan2(rho, v_z), phi = atan2(v_y, v_x) (reading R13) come from the lean
+// fm::atan2 and only supply first guesses and the local coordinates
+// u = 2 (v - v_a)/dv - 1 (values).
+//
+// Fast path: s/ds and v_z/r from one rsqrt (relative error < 1e-15 against the
+// IEEE chain); i_s and i_theta are accepted when s/ds is >= 1e-13 (s/ds + 1)
+// from an integer and v_z/r is >= 4e-15 from the boundary cosines on both sides
+// (> 100x the error bound), so they equal the contract's decisions; otherwise
+// (probability ~1e-12 per call) the exact IEEE chain decides.  The phi cross
+// products are exact IEEE products in every case.
 __device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double vy, double vz) {
     Cls c;
-    double r2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
-    c.r = __dsqrt_rn(r2);
-    double s = __ddiv_rn(L.h, c.r);
-    int is = (int)floor(__ddiv_rn(s, L.ds));
-    c.is = is > L.ns - 1 ? L.ns - 1 : is;
+    const double rho2 = __dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy));
+    const double r2 = __dadd_rn(rho2, __dmul_rn(vz, vz));
+    const double y = rsqrt(r2);
+    double s = L.h * y;
+    const double q = s * L.ids;
+    const double fq = floor(q), tq = 1e-13 * (q + 1.0);
+    int is = (int)fq;
+    bool ok;
+    if (is >= L.ns - 1) {
+        is = L.ns - 1;
+        ok = q - (double)(L.ns - 1) >= tq;
+    } else {
+        ok = (q - fq >= tq) && (fq + 1.0 - q >= tq);
+    }
     // theta: i_theta = #{k in 1..nC-1 : vz/r <= cos(k dtheta)}
-    double ct = __ddiv_rn(vz, c.r);
-    double rho = __dsqrt_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)));
-    double th = fm::atan2(rho, vz);
+    const double ct = vz * y;
+    const double rho = rho2 > 0.0 ? rho2 * rsqrt(rho2) : 0.0;
+    const double th = fm::atan2(rho, vz);
     int it = (int)(th * L.idth);
     it = it < 0 ? 0 : (it > L.nC - 1 ? L.nC - 1 : it);
-    while (it > 0 && !(ct <= __ldg(L.cos_tb + it))) --it;
-    while (it < L.nC - 1 && ct <= __ldg(L.cos_tb + it + 1)) ++it;
+    constexpr double tc = 4e-15;
+    if (it > 0 && !(ct <= __ldg(L.cos_tb + it) - tc)) ok = false;
+    if (it < L.nC - 1 && !(ct > __ldg(L.cos_tb + it + 1) + tc)) ok = false;
+    c.r = r2 * y;
+    if (!ok || L.cls_exact) {  // near a boundary: the contract's exact IEEE chain
+        c.r = __dsqrt_rn(r2);
+        s = __ddiv_rn(L.h, c.r);
+        const int ie = (int)floor(__ddiv_rn(s, L.ds));
+        is = ie > L.ns - 1 ? L.ns - 1 : ie;
+        const double cte = __ddiv_rn(vz, c.r);
+        while (it > 0 && !(cte <= __ldg(L.cos_tb + it))) --it;
+        while (it < L.nC - 1 && cte <= __ldg(L.cos_tb + it + 1)) ++it;
+    }
+    c.is = is;
     c.it = it;
     // phi: unique j with cross_j >= 0 > cross_{j+1}; poles -> 0
     const int n2 = 2 * L.nC;

@@ -627,6 +627,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         L.h = std::sqrt(3.0) / 2.0 * L.H;
         L.ds = eta / L.ns;
         L.dth = kPi / L.nC;
+        L.cls_exact = p->cls_exact;
         L.ids = 1.0 / L.ds;  // reciprocals: first guesses and local coordinates only
         L.idth = 1.0 / L.dth;
         L.ncell = 2LL * L.ns * (int64_t)L.nC * L.nC;

@@ -241,6 +241,24 @@ def test_default_kernel_choice_tc_and_staged(ifgf, nosym, monkeypatch):
     assert oracle.rel_l2(got, ref) <= PARITY
 
 
+def test_classification_fast_path_matches_exact_chain(ifgf, monkeypatch):
+    """The certified classification fast path (rsqrt-based s/ds and v_z/r with
+    margins) takes the same discrete decisions as the contract's
+    exact IEEE chain (IFGF_EXACT_CLASSIFY=1): identical relevant-segment counts,
+    fields equal up to value rounding, both at oracle parity."""
+    n, k, D = 20000, 6 * math.pi, 5
+    pts = inputs.rough_sphere(n)
+    a = inputs.densities(n, seed=13)
+    monkeypatch.setenv("IFGF_EXACT_CLASSIFY", "1")
+    _, exact, st_e = run_gpu(ifgf, pts, a, k, D)
+    monkeypatch.setenv("IFGF_EXACT_CLASSIFY", "0")
+    _, fast, st_f = run_gpu(ifgf, pts, a, k, D)
+    assert st_e["nseg"] == st_f["nseg"] and st_e["cousin_evals"] == st_f["cousin_evals"]
+    ref = oracle.OraclePlan(pts, k, D, 3, 5).apply(a)
+    assert oracle.rel_l2(exact, ref) <= PARITY and oracle.rel_l2(fast, ref) <= PARITY
+    assert oracle.rel_l2(fast, exact) <= 1e-13
+
+
 @pytest.mark.parametrize("mode,umax,leaf_nc", [("5", None, 2), ("8", None, 2), ("5", "0", 2), ("5", None, 3),
                                                ("8", None, 3)])
 def test_symmetry_orbit_grouping(ifgf, mode, umax, leaf_nc, monkeypatch):
