@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(TPB, 8) k_near(LevelParams L, const double* __
                     if (c0 + t == l) continue;
                     const double dx = x - sx[w][t], dy = y - sy[w][t], dz = z - sz[w][t];
                     const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-                    const double ri = rsqrt(r2);
+                    const double ri = fm::rsqrt_fast(r2);
                     const double r = r2 * ri;
                     double sn, cs;
                     fm::sincos(k * r, &sn, &cs);
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(TPB, 8) k_s2c(LevelParams L, const double* __r
                     const double wx = sw[t][0], wy = sw[t][1], wz = sw[t][2], ww = sw[t][3];
                     const double dx = off[0] - wx, dy = off[1] - wy, dz = off[2] - wz;
                     const double d2 = fma(dx, dx, fma(dy, dy, dz * dz));
-                    const double rdi = rsqrt(d2);
+                    const double rdi = fm::rsqrt_fast(d2);
                     const double rd = d2 * rdi;
                     // |y - x_m| - |y - c| = (w.w - 2 off.w) / (|off - w| + |off|)   (reading R17)
                     const double num = fma(-2.0, fma(off[0], wx, fma(off[1], wy, off[2] * wz)), ww);

@@ -105,6 +105,29 @@ static constexpr double kCosC_h[6] = {
 #define IFGF_FMC(name, i) name##_h[i]
 #endif
 
+// 1/sqrt(x) for finite x > 0 (values only): hardware approximation refined by one
+// third-order step y (1 + e/2 + 3e^2/8), e = 1 - x y^2 (error ~e^3: ~1 ulp), without
+// the special-case handling of the library rsqrt.
+IFGF_HD double rsqrt_fast(double x) {
+#ifdef __CUDA_ARCH__
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = std::fma(-x * y, y, 1.0);
+    return std::fma(y * e, std::fma(0.375, e, 0.5), y);
+#else
+    return 1.0 / std::sqrt(x);
+#endif
+}
+
+// Flip the sign of x when flip is true (one integer xor on the high word).
+IFGF_HD double flip_sign(double x, bool flip) {
+#ifdef __CUDA_ARCH__
+    return __hiloint2double(__double2hiint(x) ^ (flip ? (int)0x80000000 : 0), __double2loint(x));
+#else
+    return flip ? -x : x;
+#endif
+}
+
 // Shared core of atan2 / atan2_2pi: for (x, y) != (0, 0) returns p = atan(t) of the
 // reduced argument |t| <= tan(pi/8) and the octant data such that
 //   atan2(|y|, x) = k pi/4 + sg p,  k in {0, ..., 4}, sg = +-1.
@@ -159,7 +182,7 @@ IFGF_HD double atan2_core(double y, double x, int* kq, bool* neg) {
 
 IFGF_HD double octant_sum(int k, bool neg, double p) {
     const double kd = (double)k;
-    return std::fma(kd, kPi4, std::fma(kd, kPi4Lo, neg ? -p : p));
+    return std::fma(kd, kPi4, std::fma(kd, kPi4Lo, flip_sign(p, neg)));
 }
 
 // atan2(y, x) in [-pi, pi]; (x, y) != (0, 0).
@@ -215,8 +238,8 @@ IFGF_HD void sincos(double x, double* sp, double* cp) {
     const double cs = std::fma(s * s, pc, std::fma(-0.5, s, 1.0));
     const int iq = (int)(long long)q & 3;
     const double a = (iq & 1) ? cs : sn, b = (iq & 1) ? sn : cs;
-    *sp = (iq & 2) ? -a : a;
-    *cp = ((iq + 1) & 2) ? -b : b;
+    *sp = flip_sign(a, iq & 2);
+    *cp = flip_sign(b, (iq + 1) & 2);
 }
 
 }  // namespace fm

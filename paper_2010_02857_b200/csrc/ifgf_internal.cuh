@@ -207,7 +207,7 @@ struct Cls {
 //
 // Fast path: s/ds and v_z/r from one rsqrt (relative error < 1e-15 against the
 // IEEE chain); i_s and i_theta are accepted when s/ds is >= 1e-13 (s/ds + 1)
-// from an integer and v_z/r is >= 4e-15 from the boundary cosines on both sides
+// from an integer and v_z/r is >= 8e-15 from the boundary cosines on both sides
 // (> 100x the error bound), so they equal the contract's decisions; otherwise
 // (probability ~1e-12 per call) the exact IEEE chain decides.  The phi cross
 // products are exact IEEE products in every case.
@@ -215,7 +215,7 @@ __device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double 
     Cls c;
     const double rho2 = __dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy));
     const double r2 = __dadd_rn(rho2, __dmul_rn(vz, vz));
-    const double y = rsqrt(r2);
+    const double y = fm::rsqrt_fast(r2);
     double s = L.h * y;
     const double q = s * L.ids;
     const double fq = floor(q), tq = 1e-13 * (q + 1.0);
@@ -229,11 +229,11 @@ __device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double 
     }
     // theta: i_theta = #{k in 1..nC-1 : vz/r <= cos(k dtheta)}
     const double ct = vz * y;
-    const double rho = rho2 > 0.0 ? rho2 * rsqrt(rho2) : 0.0;
+    const double rho = rho2 > 0.0 ? rho2 * fm::rsqrt_fast(rho2) : 0.0;
     const double th = fm::atan2(rho, vz);
     int it = (int)(th * L.idth);
     it = it < 0 ? 0 : (it > L.nC - 1 ? L.nC - 1 : it);
-    constexpr double tc = 4e-15;
+    constexpr double tc = 8e-15;
     if (it > 0 && !(ct <= __ldg(L.cos_tb + it) - tc)) ok = false;
     if (it < L.nC - 1 && !(ct > __ldg(L.cos_tb + it + 1) + tc)) ok = false;
     c.r = r2 * y;
