@@ -214,3 +214,41 @@ def test_nodes_lie_in_their_segment(ns, nC, Ps, Pa):
         got, loc = oracle.classify(H, ns, nC, off)
         assert got == cell
         np.testing.assert_allclose(loc[:3], [ts[node[0]], ta[node[1]], ta[node[2]]], atol=1e-12)
+
+
+@pytest.mark.parametrize("ns,nC,Ps,Pa", [(1, 2, 3, 5), (4, 8, 3, 5), (8, 16, 5, 5), (2, 6, 3, 5)])
+def test_quarter_turn_tables(ns, nC, Ps, Pa):
+    """Reading R18 (n_C even): node directions come from the first-quadrant sector
+    rotated by q quarter turns.  Pins (i) the identity itself: offsets agree with
+    the unreduced spherical formula (eq. interp_pts, libm sin/cos of
+    the full angle) to rounding; (ii) exact equivariance: the node of sector
+    i_phi + n_C/2 is bit for bit (-y, x, z) of the node of sector i_phi, and a
+    vector turned by a quarter turn classifies into the sector shifted by n_C/2
+    with identical (s, theta) decisions."""
+    rng = np.random.default_rng(100 + nC)
+    H = 0.5
+    h = math.sqrt(3) / 2 * H
+    ds, dth = (math.sqrt(3) / 3) / ns, math.pi / nC
+    ts, ta = oracle.cheb_nodes(Ps), oracle.cheb_nodes(Pa)
+    for _ in range(40):
+        cell = [int(rng.integers(ns)), int(rng.integers(nC)), int(rng.integers(2 * nC))]
+        node = [int(rng.integers(Ps)), int(rng.integers(Pa)), int(rng.integers(Pa))]
+        off = oracle.node_offset(H, ns, nC, Ps, Pa, cell, node)
+        s = (cell[0] + (1 + ts[node[0]]) / 2) * ds
+        th = (cell[1] + (1 + ta[node[1]]) / 2) * dth
+        ph = (cell[2] + (1 + ta[node[2]]) / 2) * dth
+        r = h / s
+        ref = [r * math.sin(th) * math.cos(ph), r * math.sin(th) * math.sin(ph), r * math.cos(th)]
+        np.testing.assert_allclose(off, ref, rtol=0, atol=4e-15 * r)
+        if nC % 2 == 0:
+            turned = [cell[0], cell[1], (cell[2] + nC // 2) % (2 * nC)]
+            off2 = oracle.node_offset(H, ns, nC, Ps, Pa, turned, node)
+            assert off2[0] == -off[1] and off2[1] == off[0] and off2[2] == off[2]
+    for _ in range(300):
+        v = rng.normal(size=3) * H
+        c0, _ = oracle.classify(H, ns, nC, v)
+        c1, _ = oracle.classify(H, ns, nC, [-v[1], v[0], v[2]])
+        if nC % 2 == 0:
+            assert c1 == (c0[0], c0[1], (c0[2] + nC // 2) % (2 * nC))
+        else:
+            assert c1[:2] == c0[:2]
