@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(TPB, 8) k_s2c(LevelParams L, const double* __r
             }
             __syncthreads();
             if (active) {
+#pragma unroll 2
                 for (int t = 0; t < cn; ++t) {
                     const double wx = sw[t][0], wy = sw[t][1], wz = sw[t][2], ww = sw[t][3];
                     const double dx = off[0] - wx, dy = off[1] - wy, dz = off[2] - wz;
