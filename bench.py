@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 
 from paper_2010_02857_b200 import inputs  # noqa: E402
 
+ALL_CONFIGS = {**inputs.CONFIGS, **inputs.EXTRA_CONFIGS}
 METRIC = "IFGF matvec points/s (fp64 complex) at 1/2/4/8 B200; rel. error vs direct sum"
 UNIT = "points/s"
 
@@ -155,7 +156,7 @@ def run_reference(args, rank: int):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(inputs.CONFIGS[args.config], 1),
+        "config": workload_config(ALL_CONFIGS[args.config], 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -171,7 +172,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     group = dist.group.WORLD if world > 1 else None
-    c = inputs.CONFIGS[args.config]
+    c = ALL_CONFIGS[args.config]
 
     pts_h = c.points()
     a_h = c.densities()
@@ -304,7 +305,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg4", choices=sorted(inputs.CONFIGS))
+    ap.add_argument("--config", default="cfg4", choices=sorted(inputs.CONFIGS) + sorted(inputs.EXTRA_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-repeats", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

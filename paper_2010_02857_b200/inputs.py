@@ -138,3 +138,16 @@ CONFIGS = {
     "cfg4": Config("cfg4", 25_165_824, 128 * math.pi, 10, 3, 5),
     "cfg5": Config("cfg5", 100_663_296, 512 * math.pi, 12, 3, 5),
 }
+
+# SURVEY.md §8(f) workloads beyond BASELINE.json (bench.py --config; not bench defaults):
+# f1 Laplace (kappa = 0) on the cfg4 sphere; f3 the paper's 512-lambda prolate spheroid
+# (0.1, 0.1, 1) stand-in (N = 25.2 M, leaves lambda/4: D = 12) and a rough sphere at cfg4's
+# size and wavenumber.
+EXTRA_CONFIGS = {
+    "lap4": Config("lap4", 25_165_824, 0.0, 10, 3, 5, notes="f1: Laplace on the cfg4 sphere"),
+    "prolate512": Config("prolate512", 25_165_824, 512 * math.pi, 12, 3, 5, scale=(0.1, 0.1, 1.0),
+                         geometry="prolate", notes="f3: 512 lambda along z, leaves lambda/4"),
+    "rough4": Config("rough4", 25_165_824, 128 * math.pi, 10, 3, 5, geometry="rough",
+                     notes="f3: rough sphere r = 1 + 0.05 sin(40 theta) sin(40 phi)"),
+}
+

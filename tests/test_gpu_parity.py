@@ -241,6 +241,18 @@ def test_default_kernel_choice_tc_and_staged(ifgf, nosym, monkeypatch):
     assert oracle.rel_l2(got, ref) <= PARITY
 
 
+@pytest.mark.parametrize("scale", [(0.1, 0.1, 1.0), (1.0, 1.0, 0.25)])
+def test_spheroids(ifgf, scale):
+    """SURVEY.md §8(f) f3 shapes at small size: prolate (0.1, 0.1, 1) and oblate
+    (1, 1, 0.25) spheroids (segment counts and load balance differ from the sphere's)."""
+    n, k, D = 20000, 8 * math.pi, 6
+    pts = inputs.fibonacci_sphere(n, scale)
+    a = inputs.densities(n, seed=17)
+    _, got, _ = run_gpu(ifgf, pts, a, k, D)
+    ref = oracle.OraclePlan(pts, k, D, 3, 5).apply(a)
+    assert oracle.rel_l2(got, ref) <= PARITY
+
+
 def test_classification_fast_path_matches_exact_chain(ifgf, monkeypatch):
     """The certified classification fast path (rsqrt-based s/ds and v_z/r with
     margins) takes the same discrete decisions as the contract's
