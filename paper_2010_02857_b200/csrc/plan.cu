@@ -1009,6 +1009,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         };
         regroup();
         int kern = choose(per_run);
+        double per_run_orbit = sym ? per_run : 0.0;
         if (sym && !(kern == 1 || kern == 3)) {  // only the tensor-core kernels use orbits
             sym = 0;
             tile_bytes = tile_env ? std::atof(tile_env) * 1.0e6 : 4096.0e6;
@@ -1020,9 +1021,10 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         L.p.up_kernel = kern;
         L.p.sym = sym;
         if (std::getenv("IFGF_PLAN_VERBOSE"))
-            fprintf(stderr, "[ifgf] level %d: %lld boxes, nC %d ns %d, %lld segments, %lld %s runs, %.2f per run, tile %.0f MB, K7 kernel %d\n",
+            fprintf(stderr, "[ifgf] level %d: %lld boxes, nC %d ns %d, %lld segments, %lld %s runs, %.2f per run "
+                    "(orbit runs %.2f), tile %.0f MB, K7 kernel %d\n",
                     d, (long long)(L.p.b1 - L.p.b0), L.p.nC, L.p.ns, (long long)ns, (long long)nrun,
-                    sym ? "orbit" : "cell", per_run, tile_bytes / 1e6, kern);
+                    sym ? "orbit" : "cell", per_run, per_run_orbit, tile_bytes / 1e6, kern);
         k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, kern == 3 ? kChunkTC2 : (tc ? kChunkTC : kChunk), flag);
         inclusive_scan(S, flag, incl, ns, st);
         int64_t nch = d2h_one(incl + ns - 1, st);
