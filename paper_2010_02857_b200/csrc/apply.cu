@@ -76,6 +76,30 @@ __device__ __forceinline__ double rcp_nr(double x) {
     return fma(y, e, y);
 }
 
+// Warp-cooperative staging of the distinct child segments the lanes need: lanes
+// with equal slots form one group (match.any), the lowest lane of each group with
+// slot >= 0 copies its segment (one bulk copy) into buffer slot `idx` (groups in
+// lane order, at most cap); returns the lane's buffer slot, or -1 (no segment, or
+// beyond cap: the caller reads global memory).  Completion: the buffer's mbarrier
+// (expect_tx of the total bytes by lane 0).
+template <int P>
+__device__ __forceinline__ int stage_distinct(int64_t slot, int lane, int cap, const double2* __restrict__ vals,
+                                              double2* buf0, int sp, unsigned long long* bar) {
+    const unsigned grp = __match_any_sync(~0u, (unsigned long long)slot);
+    const int leader = __ffs(grp) - 1;
+    const bool lead = slot >= 0 && lane == leader;
+    const unsigned leaders = __ballot_sync(~0u, lead);
+    const int idx = __popc(leaders & ((1u << lane) - 1u));
+    const int nd = min(__popc(leaders), cap);
+    if (lead && idx < cap) {
+        fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
+        bulk_g2s(buf0 + idx * sp, vals + slot * P, P * sizeof(double2), bar);
+    }
+    if (lane == 0) mbar_arrive_expect_tx(bar, (unsigned)(nd * P * sizeof(double2)));
+    const int bi = __shfl_sync(~0u, idx, leader);
+    return (slot >= 0 && bi < cap) ? bi : -1;
+}
+
 __global__ void k_permute(const double2* __restrict__ in, const int* __restrict__ perm, int64_t n, double2* out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) out[i] = in[perm[i]];
@@ -392,7 +416,6 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
     auto prep = [&](int i, CousinEv<PS, PA>& v, int buf) {  // iteration i: cousin e0 + step i + half
         v.slot = -1;
         v.bi = -1;
-        int nd = 0;
         const int e = e0 + step * i + half;
         const int B = e < e1 ? L.cou_idx[e] : -1;
         if (active && B >= L.b0 && B < L.b1) {
@@ -410,18 +433,7 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
             v.ut = c.ut;
             v.up = c.up;
         }
-        unsigned pend = __ballot_sync(~0u, v.slot >= 0);
-        if (lane == 0) fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
-        while (pend && nd < min(SMAX, smax)) {
-            const int leader = __ffs(pend) - 1;
-            const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
-            if (lane == 0) bulk_g2s(&sbuf[w][buf][nd][0], vals + s0 * P, P * sizeof(double2), &sbar[w][buf]);
-            const bool mine = v.slot == s0;
-            if (mine) v.bi = nd;
-            pend &= ~__ballot_sync(~0u, mine);
-            ++nd;
-        }
-        if (lane == 0) mbar_arrive_expect_tx(&sbar[w][buf], (unsigned)(nd * P * sizeof(double2)));
+        v.bi = stage_distinct<P>(v.slot, lane, min(SMAX, smax), vals, &sbuf[w][buf][0][0], SP, &sbar[w][buf]);
     };
     double ar = 0.0, ai = 0.0;
     const int niter = (e1 - e0 + step - 1) / step;
@@ -519,19 +531,7 @@ __global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams
             v.ut = c.ut;
             v.up = c.up;
         }
-        unsigned pend = __ballot_sync(~0u, v.slot >= 0);
-        int nd = 0;
-        if (lane == 0) fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
-        while (pend && nd < min(SMAX, smax)) {
-            const int leader = __ffs(pend) - 1;
-            const int64_t s0 = __shfl_sync(~0u, v.slot, leader);
-            if (lane == 0) bulk_g2s(&sbuf[w][buf][nd][0], vals_d + s0 * P, P * sizeof(double2), &sbar[w][buf]);
-            const bool mine = v.slot == s0;
-            if (mine) v.bi = nd;
-            pend &= ~__ballot_sync(~0u, mine);
-            ++nd;
-        }
-        if (lane == 0) mbar_arrive_expect_tx(&sbar[w][buf], (unsigned)(nd * P * sizeof(double2)));
+        v.bi = stage_distinct<P>(v.slot, lane, min(SMAX, smax), vals_d, &sbuf[w][buf][0][0], SP, &sbar[w][buf]);
     };
     // octants with a child for some lane of the warp (the others are skipped)
     unsigned mymask = 0u;
