@@ -366,14 +366,14 @@ __global__ void k_chunk_emit(const int* __restrict__ flag, const int* __restrict
 // k-th chunks (the same boxes) at the same time.
 __global__ void k_chunk_keys(const int* __restrict__ chunk_start, int64_t nch, const int* __restrict__ cell_seg,
                              const int* __restrict__ seg_box, const int* __restrict__ seg_cell,
-                             const int* __restrict__ rsm, int64_t tile, int ch, int ns, int nC, int fs, int fc,
-                             int bsub, int bk, int bcoarse, uint64_t* key, int* val) {
+                             const int* __restrict__ rsm, int64_t tile, int ch, int ns, int nC, int hq, int fs,
+                             int fc, int bsub, int bk, int bcoarse, uint64_t* key, int* val) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nch) return;
     const int s = chunk_start[c];
     const int seg = cell_seg[s];
     const int cell = seg_cell[seg];
-    const int is = cell % ns, it = (cell / ns) % nC, ip = cell / (ns * nC);
+    const int is = cell % ns, it = (cell / ns) % nC, ip = (cell / (ns * nC)) % (hq > 0 ? hq : 2 * nC);
     const int nsc = ns / fs, ncc = nC / fc;
     const uint64_t coarse = ((uint64_t)(ip / fc) * ncc + (it / fc)) * nsc + (is / fs);
     const uint64_t sub = ((uint64_t)(ip % fc) * fc + (it % fc)) * fs + (is % fs);
@@ -1052,8 +1052,8 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
                 int* vin = S.get<int>(nch);
                 L.chunk_order = dev_alloc<int>(p, nch);
                 k_chunk_keys<<<nblocks(nch), TPB, 0, st>>>(L.chunk_start, nch, L.cell_seg, L.seg_box, L.seg_cell, rsm,
-                                                           tile, ch, L.p.ns, L.p.nC, fs, fc, bsub, bk, bcoarse, kin,
-                                                           vin);
+                                                           tile, ch, L.p.ns, L.p.nC, sym ? L.p.nC / 2 : 0, fs, fc,
+                                                           bsub, bk, bcoarse, kin, vin);
                 size_t bytes = 0;
                 const int nb = btile + bcoarse + bk + bsub;
                 IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, L.chunk_order, (int)nch, 0,
