@@ -194,12 +194,24 @@ __device__ __forceinline__ void node_off(const LevelParams& LP, int Ps, int Pa, 
 
 // K4: V[B, gamma, y] = sum_{m in B} a_m (|y-c|/|y-x_m|) e^{ik(|y-x_m| - |y-c|)}
 // (eq. factored_f P:432-434 at the nodes of eq. interp_pts), block per owned leaf.
+template <int PS, int PA>
+__device__ __forceinline__ void fit_lines_inplace(double2* V, int cnt, const int* seg, const double* Ms,
+                                                  const double* Ma, double2* out, int tid, int nt);
+
+// PS_ > 0: orders known at compile time and <= 8 segments per leaf (leaf grid
+// (1, 2)): the node values stay in shared memory and the K5 fit is fused.
 constexpr int S2C_CHUNK = 256;
+template <int PS_, int PA_>
 __global__ void __launch_bounds__(TPB, 8) k_s2c(LevelParams L, const double* __restrict__ px,
                                              const double* __restrict__ py, const double* __restrict__ pz,
                                              const double2* __restrict__ a, double k, int Ps, int Pa,
-                                             double2* vals) {
-    const int P = Ps * Pa * Pa;
+                                             double2* vals, const double* __restrict__ Ms,
+                                             const double* __restrict__ Ma) {
+    constexpr bool FUSE = PS_ > 0;
+    constexpr int PF = FUSE ? PS_ * PA_ * PA_ : 1;
+    __shared__ double2 sV[FUSE ? 8 * PF : 1];
+    __shared__ int sSeg[8];
+    const int P = FUSE ? PF : Ps * Pa * Pa;
     int64_t B = L.b0 + blockIdx.x;
     __shared__ double sw[S2C_CHUNK][4];  // source - centre (x, y, z), |source - centre|^2
     __shared__ double2 sa[S2C_CHUNK];
@@ -257,7 +269,15 @@ __global__ void __launch_bounds__(TPB, 8) k_s2c(LevelParams L, const double* __r
                 }
             }
         }
-        if (active) vals[s * P + n] = make_double2(vr, vi);
+        if (active) {
+            if constexpr (FUSE) sV[j] = make_double2(vr, vi);
+            else vals[s * P + n] = make_double2(vr, vi);
+        }
+    }
+    if constexpr (FUSE) {
+        const int cnt = (int)(s1 - s0);
+        if (threadIdx.x < cnt) sSeg[threadIdx.x] = (int)(s0 + threadIdx.x);
+        fit_lines_inplace<PS_, PA_>(sV, cnt, sSeg, Ms, Ma, vals, threadIdx.x, blockDim.x);
     }
 }
 
@@ -1889,12 +1909,24 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
     } else {
         IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));
     }
-    bool have = false;  // level d holds coefficients
+    bool have = false;        // level d holds coefficients
+    bool leaf_fused = false;  // K4 fused the leaf-level fit
     if (D >= 3 && (mask & (IFGF_STAGE_COUSIN | IFGF_STAGE_UPWARD)) && LD.p.b1 > LD.p.b0) {
         if (LD.p.nseg > 0) {
             Prof pr(p, st, 2);
-            k_s2c<<<(int)(LD.p.b1 - LD.p.b0), TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa,
-                                                             p->vals[D & 1]);
+            const unsigned nb = (unsigned)(LD.p.b1 - LD.p.b0);
+            if (LD.p.ncell <= 8 && Ps == 3 && Pa == 5) {
+                k_s2c<3, 5><<<nb, TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
+                                                p->cheb_Ms, p->cheb_Ma);
+                leaf_fused = true;
+            } else if (LD.p.ncell <= 8 && Ps == 5 && Pa == 5) {
+                k_s2c<5, 5><<<nb, TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
+                                                p->cheb_Ms, p->cheb_Ma);
+                leaf_fused = true;
+            } else {
+                k_s2c<0, 0><<<nb, TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
+                                                p->cheb_Ms, p->cheb_Ma);
+            }
             pr.done();
         }
         have = true;
@@ -1934,7 +1966,7 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
                 (double)h[10] / std::max(1.0, (double)h[12]), (double)h[11] / std::max(1.0, (double)h[12]),
                 (double)h[12] / std::max(1.0, (double)h[13]));
     };
-    if (have) fit(D);
+    if (have && !leaf_fused) fit(D);
     for (int d = D; d >= 3 && have; --d) {
         LevelParams& L = p->lev[d].p;
         const double2* vd = p->vals[d & 1];
