@@ -296,6 +296,62 @@ __global__ void k_flag_parent_nodes(LevelParams L, LevelParams LP, int Ps, int P
     }
 }
 
+// (ii'), the same flags by runs of parent segments sharing a cone cell: the
+// child-relative geometry of a parent node depends only on (cell, node, octant)
+// (DESIGN.md §7), so a warp per run classifies each (octant, node) once and sets
+// that child cell's bit in every run segment's child box of that octant (one
+// lane per distinct cell).  Same decisions as k_flag_parent_nodes, run-length
+// times fewer classifications.  sorted_seg: parent segments sorted by cell;
+// run_start: first sorted position of each run (runs cut every 32 segments).
+__global__ void k_flag_parent_runs(LevelParams L, LevelParams LP, int Ps, int Pa, const int* __restrict__ sorted_seg,
+                                   const int* __restrict__ run_start, int64_t nrun, unsigned long long* bm, int* bad) {
+    const int P = Ps * Pa * Pa;
+    const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= nrun) return;  // warp-uniform
+    const int s_begin = run_start[r];
+    const int s_end = (r + 1 < nrun) ? run_start[r + 1] : (int)LP.nseg;
+    const int cell = LP.seg_cell[sorted_seg[s_begin]];
+    // octants with a child in some run segment
+    unsigned om = 0u;
+    for (int s = s_begin + lane; s < s_end; s += 32) {
+        const int Q = LP.seg_box[sorted_seg[s]];
+        for (int o = 0; o < 8; ++o) {
+            const int B = LP.child_oct[8 * Q + o];
+            if (B >= L.b0 && B < L.b1) om |= 1u << o;
+        }
+    }
+    om = __reduce_or_sync(~0u, om);
+    const double hh = 0.5 * L.H;  // exact
+    for (int n0 = 0; n0 < P; n0 += 32) {
+        const int n = n0 + lane;
+        double off[3] = {0.0, 0.0, 0.0};
+        if (n < P) node_offset(LP, Ps, Pa, cell, n, off, nullptr);
+        for (int o = 0; o < 8; ++o) {
+            if (!((om >> o) & 1u)) continue;
+            int64_t c = -1;
+            if (n < P) {
+                const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
+                const Cls cl = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
+                c = cell_of(L, cl);
+                if (c < 0 || c >= L.ncell) {
+                    atomicOr(bad, 1);
+                    c = -1;
+                }
+            }
+            const unsigned grp = __match_any_sync(~0u, (unsigned long long)c);
+            const bool lead = c >= 0 && lane == __ffs(grp) - 1;
+            if (!__any_sync(~0u, lead)) continue;
+            for (int s = s_begin; s < s_end; ++s) {
+                const int Q = LP.seg_box[sorted_seg[s]];
+                const int B = LP.child_oct[8 * Q + o];
+                if (B < L.b0 || B >= L.b1 || !lead) continue;
+                set_bit(bm, (B - L.b0) * L.W + (c >> 6), 1ull << (c & 63));
+            }
+        }
+    }
+}
+
 __global__ void k_popc(const unsigned long long* __restrict__ bm, int64_t nw, unsigned* out) {
     int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (w >= nw) return;
@@ -351,6 +407,11 @@ __global__ void k_tile_keys(const int* __restrict__ seg_box, const int* __restri
 __global__ void k_run_start(const uint64_t* __restrict__ key, int64_t n, int* rs) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) rs[i] = (i == 0 || key[i] != key[i - 1]) ? (int)i : 0;
+}
+// run starts of a sorted key array, runs also cut every `cut` positions (bounded work per run)
+__global__ void k_key_change(const int* __restrict__ key, int64_t n, int cut, int* flag) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = (i == 0 || key[i] != key[i - 1] || i % cut == 0) ? 1 : 0;
 }
 __global__ void k_chunk_flag(const int* __restrict__ rs, int64_t n, int ch, int* flag) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -426,26 +487,40 @@ __global__ void k_stat_up(LevelParams L, LevelParams LP, int P, unsigned long lo
 }
 
 // ------------------------------------------------------------ host helpers
-struct Scratch {  // temporary device buffers freed at the end of the plan build
+// Temporary device buffers of the plan build: stream-ordered allocations from the
+// device's default memory pool (kept cached while the build runs, trimmed at the
+// end), so the many short-lived scratch arrays cost no cudaMalloc / cudaFree syncs.
+struct Scratch {
+    cudaStream_t s;
+    cudaMemPool_t pool = nullptr;
     std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t st) : s(st) {
+        int dev = 0;
+        IFGF_CUDA(cudaGetDevice(&dev));
+        IFGF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t thr = UINT64_MAX;
+        IFGF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     template <class T>
     T* get(int64_t n) {
         if (n <= 0) n = 1;
         void* p = nullptr;
-        IFGF_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)n));
+        IFGF_CUDA(cudaMallocAsync(&p, sizeof(T) * (size_t)n, s));
         ptrs.push_back(p);
         return static_cast<T*>(p);
     }
     void release(void* p) {
         for (auto& q : ptrs)
             if (q == p) {
-                cudaFree(q);
+                cudaFreeAsync(q, s);
                 q = nullptr;
             }
     }
     ~Scratch() {
         for (void* p : ptrs)
-            if (p) cudaFree(p);
+            if (p) cudaFreeAsync(p, s);
+        cudaStreamSynchronize(s);
+        if (pool) cudaMemPoolTrimTo(pool, 0);
     }
 };
 
@@ -565,7 +640,17 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         cudaStream_t s;
         ~StreamGuard() { cudaStreamDestroy(s); }
     } sg{st};
-    Scratch S;
+    Scratch S(st);
+    const bool verbose = std::getenv("IFGF_PLAN_VERBOSE") != nullptr;
+    auto t_mark = std::chrono::steady_clock::now();
+    auto step_time = [&](const char* what) {  // plan-step wall times (IFGF_PLAN_VERBOSE)
+        if (!verbose) return;
+        cudaStreamSynchronize(st);
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[ifgf] plan step %-28s %8.1f ms\n", what,
+                std::chrono::duration<double, std::milli>(t - t_mark).count());
+        t_mark = t;
+    };
 
     // 1. validation + bounding box
     {
@@ -604,6 +689,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         for (int a = 0; a < 3; ++a) p->x0[a] = p->root_c[a] - p->H1 / 2.0;
     }
 
+    step_time("1 validation+bbox");
     // 2. levels, cone grids (readings R5, R6, R8) and tables
     p->lev.assign(D + 1, LevelHost());
     for (int d = 1; d <= D; ++d) {
@@ -699,6 +785,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
     p->cheb_Ms = upload(p, cheb_fit_matrix(Ps), st);
     p->cheb_Ma = upload(p, cheb_fit_matrix(Pa), st);
 
+    step_time("2 grids+tables");
     // 3. Morton keys + radix sort (relevant boxes via integer quotients)
     uint64_t* keys_sorted = S.get<uint64_t>(n);
     {
@@ -725,6 +812,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
     k_gather_points<<<nblocks(n), TPB, 0, st>>>(pts, p->perm, n, p->px, p->py, p->pz);
     IFGF_CUDA(cudaGetLastError());
 
+    step_time("3 morton sort");
     // 4. boxes per level (leaf from points, coarser from finer)
     std::vector<uint64_t*> bkey(D + 1, nullptr);
     {
@@ -785,6 +873,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         if (d2h_one(bad, st)) throw Error{IFGF_EDOMAIN, "coincident points (the paper requires pairwise-different points)"};
     }
 
+    step_time("4 box lists");
     // 5. neighbours and cousins
     for (int d = 1; d <= D; ++d) {
         LevelHost& L = p->lev[d];
@@ -820,6 +909,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
     }
     for (int d = 1; d <= D; ++d) S.release(bkey[d]);
 
+    step_time("5 neighbours+cousins");
     // 6. source partition: owned leaf range -> owned box range per level
     {
         LevelHost& LD = p->lev[D];
@@ -877,6 +967,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         L.p.witems = L.witems;
     }
 
+    step_time("6 partition+witems");
     // 7. relevant cone segments, single sweep d = 3..D
     int* bad = S.get<int>(1);
     IFGF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
@@ -893,8 +984,51 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             k_flag_cousin_points<<<nblocks(L.p.nwitems * 32), TPB, 0, st>>>(L.p, p->px, p->py, p->pz, L.bitmap, bad);
             IFGF_CUDA(cudaGetLastError());
             if (d >= 4 && p->lev[d - 1].p.nseg > 0) {
-                LevelParams& LP = p->lev[d - 1].p;
-                k_flag_parent_nodes<<<nblocks(LP.nseg * P), TPB, 0, st>>>(L.p, LP, Ps, Pa, L.bitmap, bad);
+                LevelHost& LH = p->lev[d - 1];
+                LevelParams& LP = LH.p;
+                if (std::getenv("IFGF_FLAG_PER_NODE")) {  // A/B: one thread per (segment, node)
+                    k_flag_parent_nodes<<<nblocks(LP.nseg * P), TPB, 0, st>>>(L.p, LP, Ps, Pa, L.bitmap, bad);
+                } else {
+                    // parent segments sorted by cell, runs of equal cells, then a warp per run
+                    if (!LH.child_oct) {
+                        LH.child_oct = dev_alloc<int>(p, 8 * LP.nbox);
+                        k_child_oct<<<nblocks(LP.nbox), TPB, 0, st>>>(LH.child_start, L.box_ijk, LP.nbox, LH.child_oct);
+                        LP.child_oct = LH.child_oct;
+                    }
+                    const int64_t nsp = LP.nseg;
+                    int bits = 1;
+                    while (bits < 31 && ((int64_t)1 << bits) < LP.ncell) ++bits;
+                    int* idx_in = S.get<int>(nsp);
+                    int* idx_out = S.get<int>(nsp);
+                    int* key_in = S.get<int>(nsp);
+                    int* key_out = S.get<int>(nsp);
+                    k_iota<<<nblocks(nsp), TPB, 0, st>>>(nsp, idx_in);
+                    IFGF_CUDA(cudaMemcpyAsync(key_in, LH.seg_cell, sizeof(int) * nsp, cudaMemcpyDeviceToDevice, st));
+                    size_t bytes = 0;
+                    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key_in, key_out, idx_in, idx_out,
+                                                              (int)nsp, 0, bits, st));
+                    void* tmp = S.get<char>((int64_t)bytes);
+                    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, key_in, key_out, idx_in, idx_out, (int)nsp,
+                                                              0, bits, st));
+                    S.release(tmp);
+                    int* flag = S.get<int>(nsp);
+                    int* incl = S.get<int>(nsp);
+                    k_key_change<<<nblocks(nsp), TPB, 0, st>>>(key_out, nsp, 32, flag);
+                    inclusive_scan(S, flag, incl, nsp, st);
+                    const int64_t nrun = d2h_one(incl + nsp - 1, st);
+                    int* rstart = S.get<int>(nrun);
+                    k_chunk_emit<<<nblocks(nsp), TPB, 0, st>>>(flag, incl, nsp, rstart);
+                    k_flag_parent_runs<<<nblocks(nrun * 32), TPB, 0, st>>>(L.p, LP, Ps, Pa, idx_out, rstart, nrun,
+                                                                          L.bitmap, bad);
+                    IFGF_CUDA(cudaStreamSynchronize(st));
+                    S.release(rstart);
+                    S.release(incl);
+                    S.release(flag);
+                    S.release(key_out);
+                    S.release(key_in);
+                    S.release(idx_out);
+                    S.release(idx_in);
+                }
                 IFGF_CUDA(cudaGetLastError());
             }
         }
@@ -922,12 +1056,16 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
     }
     if (d2h_one(bad, st)) throw Error{IFGF_EINTERNAL, "classification produced a cell outside the grid"};
 
+    step_time("7 relevance");
     // 7b. K7 support: children by octant; parent segments grouped by cone cell
     for (int d = 1; d < D; ++d) {
         LevelHost& L = p->lev[d];
-        L.child_oct = dev_alloc<int>(p, 8 * L.p.nbox);
-        k_child_oct<<<nblocks(L.p.nbox), TPB, 0, st>>>(L.child_start, p->lev[d + 1].box_ijk, L.p.nbox, L.child_oct);
-        IFGF_CUDA(cudaGetLastError());
+        if (!L.child_oct) {
+            L.child_oct = dev_alloc<int>(p, 8 * L.p.nbox);
+            k_child_oct<<<nblocks(L.p.nbox), TPB, 0, st>>>(L.child_start, p->lev[d + 1].box_ijk, L.p.nbox,
+                                                            L.child_oct);
+            IFGF_CUDA(cudaGetLastError());
+        }
         L.p.child_oct = L.child_oct;
         const int64_t ns = L.p.nseg;
         if (d < 3 || ns == 0) continue;
@@ -1076,6 +1214,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         S.release(incl);
     }
 
+    step_time("7b K7 grouping");
     // 7c. multi-rank: owned-only neighbour / cousin lists and work items
     if (p->nranks > 1) {
         for (int d = 3; d <= D; ++d) {
@@ -1115,6 +1254,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         LD.p.nwitems_near = LD.p.nwitems;
     }
 
+    step_time("7c multi-rank lists");
     // 8. stats (algorithmic work units)
     {
         ifgf_stats& s = p->stats;
@@ -1155,6 +1295,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         }
     }
 
+    step_time("8 stats");
     // 9. apply scratch: permuted densities, sorted field, two segment-value levels
     p->a_sorted = dev_alloc<double2>(p, n);
     p->out_sorted = dev_alloc<double2>(p, n);
@@ -1171,6 +1312,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
     p->zseg = dev_alloc<double2>(p, P + 4);
     IFGF_CUDA(cudaMemsetAsync(p->zseg, 0, sizeof(double2) * (size_t)(P + 4), st));
     IFGF_CUDA(cudaStreamSynchronize(st));
+    step_time("9 apply buffers");
     p->stats.plan_device_bytes = p->device_bytes;
     p->stats.plan_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
