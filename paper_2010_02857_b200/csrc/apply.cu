@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
             if (v.slot < 0) atomicOr(bad, 1);
             double sn, cs;
             fm::sincos(k * c.r, &sn, &cs);
-            const double wr = kInv4Pi * rcp_nr(c.r);
+            const double wr = kInv4Pi * c.ir;
             v.gr = cs * wr;
             v.gi = sn * wr;
             v.us = c.us;

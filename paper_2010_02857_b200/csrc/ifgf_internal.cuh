@@ -193,7 +193,7 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
 // ---------------------------------------------------------------------------
 struct Cls {
     int is, it, ip;
-    double r, us, ut, up;
+    double r, ir, us, ut, up;  // ir = 1/r (value, ~1 ulp)
 };
 
 // Classification of the relative vector v at a level (DESIGN.md
@@ -237,6 +237,7 @@ __device__ __forceinline__ Cls classify(const LevelParams& L, double vx, double 
     if (it > 0 && !(ct <= __ldg(L.cos_tb + it) - tc)) ok = false;
     if (it < L.nC - 1 && !(ct > __ldg(L.cos_tb + it + 1) + tc)) ok = false;
     c.r = r2 * y;
+    c.ir = y;
     if (!ok || L.cls_exact) {  // near a boundary: the contract's exact IEEE chain
         c.r = __dsqrt_rn(r2);
         s = __ddiv_rn(L.h, c.r);
