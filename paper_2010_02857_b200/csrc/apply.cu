@@ -946,9 +946,9 @@ __device__ __forceinline__ void fit_lines_inplace(double2* V, int cnt, const int
 // K5 for the levels whose K7 writes node values (per-evaluation kernel, leaf):
 // block = 8 consecutive segments staged in shared memory, in-place line passes.
 template <int PS, int PA>
-__global__ void __launch_bounds__(128) k_fit_lines(int64_t nseg, const double* __restrict__ Ms,
-                                                   const double* __restrict__ Ma, double2* vals) {
-    constexpr int P = PS * PA * PA, NSB = 8;
+__global__ void __launch_bounds__(64) k_fit_lines(int64_t nseg, const double* __restrict__ Ms,
+                                                  const double* __restrict__ Ma, double2* vals) {
+    constexpr int P = PS * PA * PA, NSB = 4;
     __shared__ double2 sv[NSB * P];
     __shared__ int sseg[NSB];
     const int64_t s0 = (int64_t)blockIdx.x * NSB;
@@ -1939,10 +1939,10 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
         LevelParams& L = p->lev[d].p;
         if (L.nseg == 0) return;
         Prof pr(p, st, 3);
-        const unsigned nb8 = (unsigned)((L.nseg + 7) / 8);
+        const unsigned nb8 = (unsigned)((L.nseg + 3) / 4);
         dispatch(
-            Ps, Pa, [&] { k_fit_lines<3, 5><<<nb8, 128, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
-            [&] { k_fit_lines<5, 5><<<nb8, 128, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
+            Ps, Pa, [&] { k_fit_lines<3, 5><<<nb8, 64, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
+            [&] { k_fit_lines<5, 5><<<nb8, 64, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
             [&] {
                 k_fit<<<(int)((L.nseg + fit_warps - 1) / fit_warps), 32 * fit_warps, fit_smem, st>>>(
                     L.nseg, Ps, Pa, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]);
