@@ -493,15 +493,18 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
 // shared-memory slots with cp.async and every lane contracts from its slot.
 // Octant o+1 is classified and its copies issued before octant o is
 // contracted.  Output: node values (the K5 fit runs after).
+// pe block: warps and staged child segments per warp step (a warp spans 1-2 parent
+// segments, whose nodes hit up to ~6 child cells; static smem <= 48 KB per block)
+constexpr int PE_WARPS = 3, PE_SMAX = 6;
 template <int PS, int PA>
-__global__ void __launch_bounds__(128, 4) k_upward_pe(LevelParams L, LevelParams LP,
+__global__ void __launch_bounds__(PE_WARPS * 32, 5) k_upward_pe(LevelParams L, LevelParams LP,
                                                       const double2* __restrict__ vals_d, double k, double2* vals_p,
                                                       int* bad, int smax) {
     constexpr int P = PS * PA * PA;
-    constexpr int SMAX = P <= 80 ? 4 : 2;
+    constexpr int SMAX = P <= 80 ? PE_SMAX : 2;
     constexpr int SP = P + 2;
-    __shared__ __align__(16) double2 sbuf[TPB / 32][2][SMAX][SP];
-    __shared__ __align__(8) unsigned long long sbar[TPB / 32][2];
+    __shared__ __align__(16) double2 sbuf[PE_WARPS][2][SMAX][SP];
+    __shared__ __align__(8) unsigned long long sbar[PE_WARPS][2];
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if ((t & ~(int64_t)31) >= LP.nseg * P) return;  // warp-uniform
@@ -1842,7 +1845,8 @@ struct Kern {
         }
         if constexpr (PS > 0) {
             if (p->legacy_upward != 1) {
-                k_upward_pe<PS, PA><<<g, TPB, 0, st>>>(L, LP, vd, p->k, vp, bad, p->stage_slots);
+                const dim3 gpe((unsigned)((LP.nseg * (PS * PA * PA) + PE_WARPS * 32 - 1) / (PE_WARPS * 32)));
+                k_upward_pe<PS, PA><<<gpe, PE_WARPS * 32, 0, st>>>(L, LP, vd, p->k, vp, bad, p->stage_slots);
                 return false;
             }
         }
