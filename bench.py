@@ -44,13 +44,17 @@ CPU_SAMPLE_DESC = ("oracle apply (serial C++, 1 thread) on the cfg4 workload fam
                    "Fibonacci sphere N=24,576, k=4pi, D=5 (leaves lambda/4 as cfg4), (P_s,P_ang)=(3,5)")
 
 
-def algorithmic_flops_per_upward_eval(Ps: int, Pa: int) -> float:
-    """DESIGN.md §7 / SURVEY.md §8(d) ("~310 with a precomputed tensor basis"):
-    every one of the P coefficients enters one complex x real MAC (4 flops), plus
-    the recentering complex MAC (8 flops).  Geometry (classification, atan2,
-    sincos, divisions) and padding are not counted, so the fraction understates
-    the FP64 pipe's real load."""
-    return 4.0 * (Ps * Pa * Pa) + 8.0
+def algorithmic_flops_per_upward_eval(Ps: int, Pa: int, per_eval_geometry: bool = False) -> float:
+    """SURVEY.md §8(d) "Algorithmic work per unit", upward evaluation (K7) per (parent
+    node, child): "~310 with a precomputed tensor basis (P complex x real MACs), up to
+    ~460 with per-evaluation geometry".  Grouped levels (the tensor-core kernels share
+    one geometry per cell / orbit): every one of the P coefficients enters one
+    complex x real MAC (4 flops) plus the recentering complex MAC (8 flops).  Levels
+    run by the per-evaluation kernel (k_upward_pe) also compute each evaluation's
+    geometry: +152 flops (460 - 308 at P = 75).  Special functions (sqrt, division,
+    atan2, sincos) and padding are not counted, so the fraction understates the
+    FP64 pipe's real load."""
+    return 4.0 * (Ps * Pa * Pa) + 8.0 + (152.0 if per_eval_geometry else 0.0)
 
 
 class ClockSampler:
@@ -258,7 +262,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ---------------- roofline of the dominant kernel (K7 upward, FP64 pipe)
     up_ms, up_launch = prof["upward"]
     up_evals = sum(st["upward_evals"].values())  # per apply (this rank)
-    flops_apply = up_evals * algorithmic_flops_per_upward_eval(c.Ps, c.Pang)
+    # per level: kernel 2 (k_upward_pe) computes the geometry per evaluation
+    pe_evals = sum(v for d, v in st["upward_evals"].items() if st["upward_kernel"].get(d, -1) == 2)
+    flops_apply = ((up_evals - pe_evals) * algorithmic_flops_per_upward_eval(c.Ps, c.Pang)
+                   + pe_evals * algorithmic_flops_per_upward_eval(c.Ps, c.Pang, True))
     achieved = flops_apply * args.steps / (up_ms * 1e-3) if up_ms > 0 else 0.0
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -289,8 +296,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "traffic": traffic,
                          "peak_source": "FP64 DFMA microbenchmark (ifgf_bench_dfma) measured in this run; "
                                         "nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s",
-                         "flops_per_unit": algorithmic_flops_per_upward_eval(c.Ps, c.Pang),
-                         "units_per_step": up_evals},
+                         "flops_per_unit": {"grouped_geometry": algorithmic_flops_per_upward_eval(c.Ps, c.Pang),
+                                            "per_evaluation_geometry":
+                                                algorithmic_flops_per_upward_eval(c.Ps, c.Pang, True)},
+                         "units_per_step": {"grouped_geometry": up_evals - pe_evals,
+                                            "per_evaluation_geometry": pe_evals},
+                         "flops_per_step": flops_apply},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * c.n, "d2h_bytes_per_step": 16 * c.n},
             "gpu_launches": launches,
             "clocks": clk,
