@@ -77,6 +77,24 @@ def test_cfg1_plan_diff(cfg1_runs):
         np.testing.assert_array_equal(segs_sorted(plan.level_segments(d)), segs_sorted(oplan.level_segments(d)))
 
 
+def test_plan_flags_by_runs_match_per_node(ifgf, monkeypatch):
+    """The plan's relevance flags by runs of parent segments sharing a cell (one
+    classification per (cell, node, octant)) give exactly the per-(segment, node)
+    flags (IFGF_FLAG_PER_NODE=1): identical segment lists at every level, on a
+    rough sphere with long and short runs, and the oracle's lists too."""
+    n, k, D = 30000, 8 * math.pi, 6
+    pts = inputs.rough_sphere(n)
+    monkeypatch.setenv("IFGF_FLAG_PER_NODE", "1")
+    per_node = ifgf.Plan(dev(pts), k, D, 3, 5)
+    monkeypatch.delenv("IFGF_FLAG_PER_NODE")
+    runs = ifgf.Plan(dev(pts), k, D, 3, 5)
+    oplan = oracle.OraclePlan(pts, k, D, 3, 5)
+    for d in range(3, D + 1):
+        a = segs_sorted(runs.level_segments(d))
+        np.testing.assert_array_equal(a, segs_sorted(per_node.level_segments(d)))
+        np.testing.assert_array_equal(a, segs_sorted(oplan.level_segments(d)))
+
+
 def test_cfg1_stage_masks(cfg1_runs, ifgf):
     c, pts, a, oplan, ref, plan, got, st = cfg1_runs
     for mask in (ifgf.IFGF_STAGE_NEAR, ifgf.IFGF_STAGE_NEAR | ifgf.IFGF_STAGE_COUSIN, ifgf.IFGF_STAGE_COUSIN):
