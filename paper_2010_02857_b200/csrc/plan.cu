@@ -1132,6 +1132,8 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             if (p->legacy_upward == 8) kn = 3;                           // force the tensor-core kernel v2
             if (P > 80 && kn == 1) kn = 0;  // TC kernel shared memory is sized for P <= 80 ((P_s, P_ang) = (3, 5))
             if (kn == 3 && !(Ps == 3 && Pa == 5)) kn = 1;  // TC v2 k-permutation is specific to (3, 5)
+            // orders without a compiled specialisation run the generic per-evaluation kernel
+            if (!((Ps == 3 && Pa == 5) || (Ps == 5 && Pa == 5))) kn = 2;
             return kn;
         };
         int64_t nrun = 0;
