@@ -271,6 +271,23 @@ def test_spheroids(ifgf, scale):
     assert oracle.rel_l2(got, ref) <= PARITY
 
 
+@pytest.mark.slow
+def test_cfg3_family_oblate_p55(ifgf):
+    """cfg3's workload family at 1/16 of its size: oblate (1, 1, 0.25) spheroid, leaves
+    lambda/2, (P_s, P_ang) = (5, 5) (the P = 125 specialised kernels), N = 98,304,
+    k = 8 pi, D = 5: parity with the oracle, and the error against the direct sum
+    within 1.1x the oracle's."""
+    n, k, D = 98_304, 8 * math.pi, 5
+    pts = inputs.fibonacci_sphere(n, (1.0, 1.0, 0.25))
+    a = inputs.densities(n)
+    ref = oracle.OraclePlan(pts, k, D, 5, 5).apply(a)
+    _, got, _ = run_gpu(ifgf, pts, a, k, D, 5, 5)
+    assert oracle.rel_l2(got, ref) <= PARITY
+    tg = inputs.error_targets(n, 1000)
+    exact = ifgf.direct(dev(pts), k, dev(a), dev(tg)).cpu().numpy()
+    assert oracle.rel_l2(got[tg], exact) <= 1.1 * oracle.rel_l2(ref[tg], exact)
+
+
 def test_classification_fast_path_matches_exact_chain(ifgf, monkeypatch):
     """The certified classification fast path (rsqrt-based s/ds and v_z/r with
     margins) takes the same discrete decisions as the contract's
