@@ -163,10 +163,10 @@ struct ifgf_plan_s {
     int legacy_upward = 0;   // env IFGF_LEGACY_UPWARD: K7 variant override (A/B testing, tests)
     int no_symmetry = 0;     // env IFGF_NO_SYMMETRY: K7 chunks by cell only (A/B testing, tests)
     int cls_exact = 0;       // env IFGF_EXACT_CLASSIFY: no classification fast path (tests)
-    int tc_umax = 1 << 30;
+    int tc_umax = 1 << 30;      // env IFGF_TC_UMAX: cap on staged child cells in the TC K7 (tests the fallback)
     int stage_slots = 1 << 30;  // env IFGF_STAGE_SLOTS: cap on staged child segments per warp in K6 / K7-pe (tests)
-    int legacy_cousin = 0;   // env IFGF_LEGACY_COUSIN=1: per-lane global-load K6 (A/B testing)
-    unsigned long long* phase_clk = nullptr;  // env IFGF_PHASE_PROF: TC K7 per-phase clock sums   // env IFGF_TC_UMAX: cap on staged child cells in the TC K7 (tests the fallback)
+    int legacy_cousin = 0;      // env IFGF_LEGACY_COUSIN=1: per-lane global-load K6 (A/B testing)
+    unsigned long long* phase_clk = nullptr;  // env IFGF_PHASE_PROF: TC K7 per-phase clock sums
     int64_t device_bytes = 0;
     std::vector<void*> allocs;  // every cudaMalloc of the plan
 };
