@@ -1803,12 +1803,9 @@ struct Kern {
         if constexpr (PS == 3 && PA == 5) {
             if (LP.up_kernel == 3 && LP.nchunk > 0) {
                 using Cfg = Tc2Cfg<PS, PA>;
-                static bool attr = false;
-                if (!attr) {
-                    IFGF_CUDA(cudaFuncSetAttribute(k_upward_tc2<PS, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)Cfg::smem));
-                    attr = true;
-                }
+                // per launch (cheap): the attribute is per device, and a process may drive several
+                IFGF_CUDA(cudaFuncSetAttribute(k_upward_tc2<PS, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)Cfg::smem));
                 k_upward_tc2<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(
                     L, LP, vd, p->k, p->cheb_Ms, p->cheb_Ma, vp, bad, std::min(Cfg::UM, p->tc_umax), p->zseg);
                 return true;
@@ -1817,12 +1814,9 @@ struct Kern {
         if constexpr (PS > 0 && PS * PA * PA <= 80) {
             if (LP.up_kernel == 1 && LP.nchunk > 0) {
                 using Cfg = TcCfg<PS, PA>;
-                static bool attr = false;
-                if (!attr) {
-                    IFGF_CUDA(cudaFuncSetAttribute(k_upward_tc<PS, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)Cfg::smem));
-                    attr = true;
-                }
+                // per launch (cheap): the attribute is per device, and a process may drive several
+                IFGF_CUDA(cudaFuncSetAttribute(k_upward_tc<PS, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)Cfg::smem));
                 k_upward_tc<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(
                     L, LP, vd, p->k, p->cheb_Ms, p->cheb_Ma, vp, bad, std::min(Cfg::UM, p->tc_umax), p->zseg,
                     p->phase_clk);
@@ -1832,12 +1826,9 @@ struct Kern {
         if constexpr (PS > 0 && PS * PA * PA <= 128) {
             if (LP.up_kernel == 0 && LP.nchunk > 0) {
                 using Cfg = StagedCfg<PS, PA>;
-                static bool attr = false;
-                if (!attr) {
-                    IFGF_CUDA(cudaFuncSetAttribute(k_upward_s<PS, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)Cfg::smem));
-                    attr = true;
-                }
+                // per launch (cheap): the attribute is per device, and a process may drive several
+                IFGF_CUDA(cudaFuncSetAttribute(k_upward_s<PS, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)Cfg::smem));
                 k_upward_s<PS, PA><<<(unsigned)LP.nchunk, Cfg::NT, Cfg::smem, st>>>(L, LP, vd, p->k, p->cheb_Ms,
                                                                                       p->cheb_Ma, vp, bad);
                 return true;
