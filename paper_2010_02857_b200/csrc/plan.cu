@@ -1085,6 +1085,9 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             (double)p->lev[d + 1].p.nseg * P * 16.0 / (double)std::max<int64_t>(1, L.p.b1 - L.p.b0);
         double tile_bytes = 4096.0e6;  // child bytes per tile (env IFGF_TILE_MB: fixed)
         const char* tile_env = std::getenv("IFGF_TILE_MB");
+        // adaptive tiles: aim at ~tile_target segments per run where runs are very long
+        const double tile_target = std::getenv("IFGF_TILE_TARGET") ? std::atof(std::getenv("IFGF_TILE_TARGET")) : 256.0;
+        const double tile_min = std::getenv("IFGF_TILE_MIN_MB") ? std::atof(std::getenv("IFGF_TILE_MIN_MB")) * 1e6 : 32.0e6;
         if (tile_env) tile_bytes = std::atof(tile_env) * 1.0e6;
         int* rs = S.get<int>(ns);
         int* rsm = S.get<int>(ns);
@@ -1141,8 +1144,8 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         auto regroup = [&]() {
             nrun = group(tile_bytes);
             per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
-            if (!tile_env && per_run > 1024.0) {
-                tile_bytes = std::max(32.0e6, tile_bytes * 256.0 / per_run);
+            if (!tile_env && per_run > 4.0 * tile_target) {
+                tile_bytes = std::max(tile_min, tile_bytes * tile_target / per_run);
                 nrun = group(tile_bytes);
                 per_run = (double)ns / (double)std::max<int64_t>(1, nrun);
             }
