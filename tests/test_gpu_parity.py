@@ -222,6 +222,22 @@ def test_multirank_emulation_one_gpu(ifgf):
         assert oracle.rel_l2(acc, full) < 1e-13, R
 
 
+def test_multirank_emulation_tc_orbits(ifgf):
+    """Source partition on a case whose fine levels run the tensor-core K7 with
+    quarter-turn orbits: the per-rank partial fields (3 ranks, sequentially on one GPU)
+    sum to the single-GPU field."""
+    n, k, D = 60000, 8 * math.pi, 6
+    pts = inputs.fibonacci_sphere(n)
+    a = inputs.densities(n, seed=21)
+    _, full, st = run_gpu(ifgf, pts, a, k, D)
+    assert st["upward_kernel"][D] == 1
+    acc = np.zeros_like(full)
+    for r in range(3):
+        _, part, _ = run_gpu(ifgf, pts, a, k, D, rank=r, nranks=3)
+        acc += part
+    assert oracle.rel_l2(acc, full) < 1e-13
+
+
 @pytest.mark.parametrize("legacy,slots", [("0", None), ("0", "1"), ("0", "0"), ("1", None)])
 def test_cousin_kernel_variants(ifgf, legacy, slots, monkeypatch):
     """K6: the warp-staged kernel (default) and the per-lane global-load kernel
