@@ -83,9 +83,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // beyond cap: the caller reads global memory).  Completion: the buffer's mbarrier
 // (expect_tx of the total bytes by lane 0).
 template <int P>
-__device__ __forceinline__ int stage_distinct(int64_t slot, int lane, int cap, const double2* __restrict__ vals,
+__device__ __forceinline__ int stage_distinct(int slot, int lane, int cap, const double2* __restrict__ vals,
                                               double2* buf0, int sp, unsigned long long* bar) {
-    const unsigned grp = __match_any_sync(~0u, (unsigned long long)slot);
+    const unsigned grp = __match_any_sync(~0u, slot);
     const int leader = __ffs(grp) - 1;
     const bool lead = slot >= 0 && lane == leader;
     const unsigned leaders = __ballot_sync(~0u, lead);
@@ -93,7 +93,7 @@ __device__ __forceinline__ int stage_distinct(int64_t slot, int lane, int cap, c
     const int nd = min(__popc(leaders), cap);
     if (lead && idx < cap) {
         fence_proxy_async();  // the buffer's previous contents were read (generic proxy)
-        bulk_g2s(buf0 + idx * sp, vals + slot * P, P * sizeof(double2), bar);
+        bulk_g2s(buf0 + idx * sp, vals + (int64_t)slot * P, P * sizeof(double2), bar);
     }
     if (lane == 0) mbar_arrive_expect_tx(bar, (unsigned)(nd * P * sizeof(double2)));
     const int bi = __shfl_sync(~0u, idx, leader);
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(TPB) k_cousin(LevelParams L, const double* __r
 // contracted (double-buffered slots), hiding the global-memory latency.
 template <int PS, int PA>
 struct CousinEv {
-    int64_t slot;  // segment slot (-1: none)
+    int slot;  // segment slot (-1: none; a level has < 2^31 segments)
     int bi;        // shared-memory slot index, -1 if beyond SMAX (global fallback)
     double gr, gi, us, ut, up;
 };
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
             double cx, cy, cz;
             box_centre3(L, B, cx, cy, cz);
             const Cls c = classify(L, __dsub_rn(x, cx), __dsub_rn(y, cy), __dsub_rn(z, cz));
-            v.slot = seg_slot(L, B, cell_of(L, c));
+            v.slot = (int)seg_slot(L, B, cell_of(L, c));
             if (v.slot < 0) atomicOr(bad, 1);
             double sn, cs;
             fm::sincos(k * c.r, &sn, &cs);
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
             double Ts[PS], Tt[2] = {1.0, cur.ut};  // contract_sm_lr needs T_0, T_1 of u_theta only
             cheb_T<PS>(cur.us, Ts);
             const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA, false, PA>(&sbuf[w][cb][cur.bi][0], Ts, Tt, cur.up)
-                                          : contract_sm_lr<PS, PA>(vals + cur.slot * P, Ts, Tt, cur.up);
+                                          : contract_sm_lr<PS, PA>(vals + (int64_t)cur.slot * P, Ts, Tt, cur.up);
             ar = fma(cur.gr, F.x, fma(-cur.gi, F.y, ar));
             ai = fma(cur.gr, F.y, fma(cur.gi, F.x, ai));
         }
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(PE_WARPS * 32, 5) k_upward_pe(LevelParams L, L
     const double rQ = sqrt(fma(off[0], off[0], fma(off[1], off[1], off[2] * off[2])));
     const double hh = 0.5 * L.H;
     struct Ev {
-        int64_t slot;
+        int slot;  // a level has < 2^31 segments
         int bi;
         double rr, ri, us, ut, up;
     };
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(PE_WARPS * 32, 5) k_upward_pe(LevelParams L, L
         if (B >= 0) {
             const double dx = (o & 4) ? -hh : hh, dy = (o & 2) ? -hh : hh, dz = (o & 1) ? -hh : hh;
             const Cls c = classify(L, __dadd_rn(off[0], dx), __dadd_rn(off[1], dy), __dadd_rn(off[2], dz));
-            v.slot = seg_slot(L, B, cell_of(L, c));
+            v.slot = (int)seg_slot(L, B, cell_of(L, c));
             if (v.slot < 0) atomicOr(bad, 1);
             // r_B - r_Q = (delta.delta + 2 off.delta) / (r_B + r_Q)   (reading R17)
             const double num =
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(PE_WARPS * 32, 5) k_upward_pe(LevelParams L, L
             cheb_T<PS>(cur.us, Ts);
             cheb_T<PA>(cur.ut, Tt);
             const double2 F = cur.bi >= 0 ? contract_sm_lr<PS, PA, false, PA>(&sbuf[w][cb][cur.bi][0], Ts, Tt, cur.up)
-                                          : contract_sm_lr<PS, PA, true>(vals_d + cur.slot * P, Ts, Tt, cur.up);
+                                          : contract_sm_lr<PS, PA, true>(vals_d + (int64_t)cur.slot * P, Ts, Tt, cur.up);
             ar = fma(cur.rr, F.x, fma(-cur.ri, F.y, ar));
             ai = fma(cur.rr, F.y, fma(cur.ri, F.x, ai));
         }
