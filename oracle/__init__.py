@@ -23,7 +23,7 @@ ST_NEAR, ST_COUSIN, ST_UPWARD = 1, 2, 4
 ST_ALL = 7
 MODE_NORMAL, MODE_BYPASS = 0, 1
 
-CFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+CFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC"]
 
 
 def build(force: bool = False) -> str:
@@ -44,6 +44,8 @@ def lib():
             c_d, c_i, c_i64, c_p = ctypes.c_double, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
             L.oracle_plan_create.argtypes = [c_p, c_i64, c_d, c_i, c_i, c_i, c_i, c_i, c_i, c_p, c_d,
                                              ctypes.POINTER(c_p)]
+            L.oracle_plan_create_part.argtypes = [c_p, c_i64, c_d, c_i, c_i, c_i, c_i, c_i, c_i, c_p, c_d,
+                                                  ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(c_p)]
             L.oracle_plan_destroy.argtypes = [c_p]
             L.oracle_apply.argtypes = [c_p, c_p, c_p, ctypes.c_uint, c_i]
             L.oracle_recentering_check.argtypes = [c_p, c_p]
@@ -66,8 +68,21 @@ def lib():
             L.oracle_tensor_eval.argtypes = [c_i, c_i, c_p, c_d, c_d, c_d, c_p]
             L.oracle_classify.argtypes = [c_d, c_i, c_i, c_p, c_p, c_p]
             L.oracle_node_offset.argtypes = [c_d, c_i, c_i, c_i, c_i, c_p, c_p, c_p]
+            L.oracle_set_threads.argtypes = [c_i]
+            L.oracle_get_threads.restype = c_i
             _lib = L
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Threads of the oracle's parallel loops (0 = all processors, 1 = serial).
+    Results are bitwise independent of it (target- / parent-segment-major loops
+    with one owner per output; oracle/ifgf_oracle.cpp header)."""
+    lib().oracle_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().oracle_get_threads())
 
 
 def _ptr(a: np.ndarray):
@@ -91,20 +106,24 @@ class OracleError(RuntimeError):
 class OraclePlan:
     """Oracle plan: box tree, cone grids and relevant segments."""
 
-    def __init__(self, points, k, levels, Ps, Pang, leaf_ns=1, leaf_nc=2, root=None):
+    def __init__(self, points, k, levels, Ps, Pang, leaf_ns=1, leaf_nc=2, root=None, owned_morton=None):
+        """owned_morton: optional half-open range (lo, hi) of leaf Morton keys whose
+        sources this plan owns (source partition); apply() then
+        returns the partial field over all targets."""
         L = lib()
         self.points = _f64(points).reshape(-1, 3)
         self.n = self.points.shape[0]
         self.D, self.Ps, self.Pang = int(levels), int(Ps), int(Pang)
         self.k = float(k)
+        lo, hi = (0, 2 ** 64 - 1) if owned_morton is None else (int(owned_morton[0]), int(owned_morton[1]))
         h = ctypes.c_void_p()
         if root is not None:
             rc = _f64(root[0])
-            st = L.oracle_plan_create(_ptr(self.points), self.n, self.k, self.D, self.Ps, self.Pang, leaf_ns,
-                                      leaf_nc, 1, _ptr(rc), float(root[1]), ctypes.byref(h))
+            st = L.oracle_plan_create_part(_ptr(self.points), self.n, self.k, self.D, self.Ps, self.Pang, leaf_ns,
+                                           leaf_nc, 1, _ptr(rc), float(root[1]), lo, hi, ctypes.byref(h))
         else:
-            st = L.oracle_plan_create(_ptr(self.points), self.n, self.k, self.D, self.Ps, self.Pang, leaf_ns,
-                                      leaf_nc, 0, None, 0.0, ctypes.byref(h))
+            st = L.oracle_plan_create_part(_ptr(self.points), self.n, self.k, self.D, self.Ps, self.Pang, leaf_ns,
+                                           leaf_nc, 0, None, 0.0, lo, hi, ctypes.byref(h))
         if st != 0:
             raise OracleError(st, "oracle_plan_create")
         self._h = h
