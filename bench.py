@@ -7,11 +7,13 @@ complex) at 1/2/4/8 B200; rel. error vs direct sum").
 
 One step = one full IFGF operator application (the whole hot path: permute,
 near field, source-to-cone, per-level fit / cousin / upward, un-permute; plus
-the NCCL all-reduce of the partial fields when N > 1) on synthetic inputs
-resident in HBM.  Prints ONE JSON line on rank 0.
+the in-library NCCL all-reduce of the partial fields when N > 1) on synthetic
+inputs resident in HBM.  Prints ONE JSON line on rank 0.
 
---impl reference times the oracle (oracle/, serial C++) on a bounded sample of
-the same workload family on the host cores (rank 0 only).
+--impl reference times the oracle (oracle/, C++ with its deterministic OpenMP
+mode on all host cores) on a bounded sample of the same workload: the partial
+apply of a 1/256 Morton slice of the leaves (sources) over all N targets,
+extrapolated by the slice's share of the sources (rank 0 only).
 """
 from __future__ import annotations
 
@@ -36,12 +38,50 @@ ALL_CONFIGS = {**inputs.CONFIGS, **inputs.EXTRA_CONFIGS}
 METRIC = "IFGF matvec points/s (fp64 complex) at 1/2/4/8 B200; rel. error vs direct sum"
 UNIT = "points/s"
 
-# Bounded CPU sample for the oracle (cpu_baseline and --impl reference): the same
-# workload family as cfg4 (Fibonacci sphere, 22 points per wavelength, leaves of
-# lambda/4, (P_s, P_ang) = (3, 5)) scaled down to 4 lambda: N = 24,576, k = 4 pi, D = 5.
-CPU_SAMPLE = dict(n=24_576, k=4 * math.pi, levels=5, Ps=3, Pang=5)
-CPU_SAMPLE_DESC = ("oracle apply (serial C++, 1 thread) on the cfg4 workload family scaled to 4 lambda: "
-                   "Fibonacci sphere N=24,576, k=4pi, D=5 (leaves lambda/4 as cfg4), (P_s,P_ang)=(3,5)")
+# Bounded CPU sample of the oracle (cpu_baseline and --impl reference): the oracle
+# plan of the SAME workload owning a contiguous Morton slice of 1/256 of the leaf
+# boxes (source partition); one step = its partial apply over all
+# N targets; points/s = (owned sources / N) * N / t, i.e. the full apply's rate if
+# its time scaled with the sources (coarse ancestors of the slice are shared, so
+# the slice costs a little more than 1/256: a conservative estimate).
+CPU_SLICE = (0.45, 1.0 / 256)
+
+
+class OracleSample:
+    def __init__(self, c):
+        import oracle
+        oracle.set_threads(0)
+        self.cores = oracle.get_threads()
+        self.c = c
+        pts = c.points()
+        self.a = c.densities()
+        t0 = time.perf_counter()
+        tree = oracle.OraclePlan(pts, c.k, c.levels, c.Ps, c.Pang, owned_morton=(0, 0))  # tree only
+        info = tree.level_info(c.levels)
+        del tree
+        q = np.clip(np.floor((pts - info["x0"]) / info["H"]), 0, 2 ** (c.levels - 1) - 1).astype(np.uint64)
+        key = np.zeros(len(pts), dtype=np.uint64)
+        for bit in range(21):
+            for ax, sh in ((0, 2), (1, 1), (2, 0)):
+                key |= ((q[:, ax] >> np.uint64(bit)) & np.uint64(1)) << np.uint64(3 * bit + sh)
+        leaves = np.unique(key)
+        i0 = int(CPU_SLICE[0] * len(leaves))
+        i1 = i0 + max(1, int(CPU_SLICE[1] * len(leaves)))
+        lo, hi = int(leaves[i0]), int(leaves[min(i1, len(leaves) - 1)])
+        self.frac = float(np.mean((key >= np.uint64(lo)) & (key < np.uint64(hi))))
+        self.plan = oracle.OraclePlan(pts, c.k, c.levels, c.Ps, c.Pang, owned_morton=(lo, hi))
+        self.setup_s = time.perf_counter() - t0
+        self.desc = (f"oracle (C++, deterministic OpenMP on {self.cores} host threads) partial apply of "
+                     f"{c.name} over all N={c.n} targets from a Morton slice of {i1 - i0} of {len(leaves)} leaf "
+                     f"boxes ({self.frac * 100:.3f}% of the sources); points/s = (slice sources / N) * N / t")
+
+    def step(self) -> float:
+        t0 = time.perf_counter()
+        self.plan.apply(self.a)
+        return time.perf_counter() - t0
+
+    def value(self, t: float) -> float:
+        return self.frac * self.c.n / t
 
 
 def algorithmic_flops_per_upward_eval(Ps: int, Pa: int, per_eval_geometry: bool = False) -> float:
@@ -115,20 +155,6 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
-def time_oracle_sample(repeats: int = 1):
-    import oracle
-    c = CPU_SAMPLE
-    pts = inputs.fibonacci_sphere(c["n"])
-    a = inputs.densities(c["n"])
-    plan = oracle.OraclePlan(pts, c["k"], c["levels"], c["Ps"], c["Pang"])
-    ts = []
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        plan.apply(a)
-        ts.append(time.perf_counter() - t0)
-    return c["n"], ts
-
-
 def workload_config(c, world: int, st=None) -> dict:
     """The `config` object of the JSON line (same for both arms)."""
     cfg = {
@@ -136,8 +162,8 @@ def workload_config(c, world: int, st=None) -> dict:
                     f"N={c.n}, D={c.levels}, (P_s,P_ang)=({c.Ps},{c.Pang}), Fibonacci points, "
                     "splitmix64 densities",
         "N": c.n, "k": c.k, "levels": c.levels, "P_s": c.Ps, "P_ang": c.Pang,
-        "parallelism": f"source-partition x{world} (Morton leaf ranges) + NCCL all-reduce" if world > 1
-        else "1 GPU",
+        "parallelism": f"source-partition x{world} (work-weighted Morton leaf ranges) + in-library NCCL "
+                       "all-reduce" if world > 1 else "1 GPU",
     }
     if st is not None:
         cfg["l2"] = ("inputs larger than L2: each apply streams "
@@ -146,22 +172,24 @@ def workload_config(c, world: int, st=None) -> dict:
 
 
 def run_reference(args, rank: int):
-    """Reference arm: the oracle (serial C++ CPU IFGF) timed as it stands on a bounded
-    sample of the same workload family (the full cfg4 apply would take ~35 min on one
-    core); the line carries our arm's config, metric and unit."""
+    """Reference arm: the oracle (C++ CPU IFGF, deterministic OpenMP on all host
+    cores) as it stands, each step the partial apply of the bounded cfg slice
+    (OracleSample); the line carries our arm's config, metric and unit."""
     if rank != 0:
         return
-    n, ts = time_oracle_sample(args.warmup + args.steps)
+    c = ALL_CONFIGS[args.config]
+    smp = OracleSample(c)
+    ts = [smp.step() for _ in range(args.warmup + args.steps)]
     timed = ts[args.warmup:] if len(ts) > args.warmup else ts
     t = sum(timed) / len(timed)
-    value = n / t
-    sample = CPU_SAMPLE_DESC + f"; {len(timed)} timed applies after {args.warmup} warm-up"
+    value = smp.value(t)
+    sample = smp.desc + f"; mean of {len(timed)} timed steps after {args.warmup} warm-up"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(ALL_CONFIGS[args.config], 1),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "config": workload_config(c, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": smp.cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -175,7 +203,6 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    group = dist.group.WORLD if world > 1 else None
     c = ALL_CONFIGS[args.config]
 
     pts_h = c.points()
@@ -186,8 +213,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     dfma_flops, _ = ifgf.bench_dfma(20000)  # measured FP64 FMA peak (roofline denominator)
 
+    comm = ifgf.NcclComm.from_group(None, local_rank) if world > 1 else None
     t0 = time.perf_counter()
-    plan = ifgf.Plan(pts, c.k, c.levels, c.Ps, c.Pang, rank=rank, nranks=world, group=group)
+    plan = ifgf.Plan(pts, c.k, c.levels, c.Ps, c.Pang, rank=rank, nranks=world, comm=comm)
     torch.cuda.synchronize()
     plan_s = time.perf_counter() - t0
     st = plan.stats()
@@ -219,6 +247,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     ms = e0.elapsed_time(e1)
     prof = plan.profile_read(reset=True)
     plan.profile_enable(False)
+    plan.stats()  # raises IfgfError if an apply met an invariant violation
     t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
@@ -229,8 +258,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ---------------- end to end: host buffers in, host result out, every step
     a_pin = torch.from_numpy(a_h).pin_memory()
     out_pin = torch.empty(c.n, dtype=torch.complex128).pin_memory()
-    if world == 1:
-        plan.apply_host(a_pin, out_pin)  # warm
+    plan.apply_host(a_pin, out_pin)  # warm
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -238,13 +266,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for _ in range(args.steps):
-        if world == 1:
-            plan.apply_host(a_pin, out_pin)  # C ABI: H2D, apply, D2H, sync
-        else:
-            a_dev = a_pin.to(dev, non_blocking=True)
-            plan.apply(a_dev, out)  # includes the NCCL all-reduce
-            out_pin.copy_(out, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+        plan.apply_host(a_pin, out_pin)  # C ABI: H2D, apply (+ NCCL all-reduce when N > 1), D2H, sync
     e3.record(stream)
     torch.cuda.synchronize()
     te = torch.tensor([e2.elapsed_time(e3)], dtype=torch.float64, device=dev)
@@ -258,6 +280,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     exact = ifgf.direct(pts, c.k, a, tg)
     got = out[tg]
     rel_err = float(torch.sqrt(torch.sum(torch.abs(got - exact) ** 2) / torch.sum(torch.abs(exact) ** 2)).item())
+    st_after = plan.stats()  # raises IfgfError if an apply met an invariant violation
 
     # ---------------- roofline of the dominant kernel (K7 upward, FP64 pipe)
     up_ms, up_launch = prof["upward"]
@@ -280,9 +303,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            n_s, ts = time_oracle_sample(args.cpu_repeats)
-            cpu = {"value": n_s / statistics.median(ts), "unit": UNIT, "cores": 1, "kind": "oracle",
-                   "sample": CPU_SAMPLE_DESC + f"; median of {len(ts)} applies ({sum(ts):.1f} s of CPU work)"}
+            smp = OracleSample(c)
+            ts = [smp.step() for _ in range(args.cpu_repeats)]
+            cpu = {"value": smp.value(statistics.median(ts)), "unit": UNIT, "cores": smp.cores, "kind": "oracle",
+                   "sample": smp.desc + f"; median of {len(ts)} steps ({sum(ts):.1f} s wall, after "
+                                        f"{smp.setup_s:.0f} s of oracle plan set-up)"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -304,6 +329,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "flops_per_step": flops_apply},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * c.n, "d2h_bytes_per_step": 16 * c.n},
             "gpu_launches": launches,
+            "graph_applies": st_after["graph_applies"],
             "clocks": clk,
         }
         if cpu is not None:
@@ -318,7 +344,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4", choices=sorted(inputs.CONFIGS) + sorted(inputs.EXTRA_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-repeats", type=int, default=3)
+    ap.add_argument("--cpu-repeats", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -44,7 +44,8 @@ typedef enum {
     IFGF_EDOMAIN = 2,   /* coincident points or a zero-extent cloud with n > 1 */
     IFGF_ENOMEM = 3,    /* device or host allocation failed; partial state freed         */
     IFGF_ECUDA = 4,     /* CUDA runtime error (sticky)                                   */
-    IFGF_ENCCL = 5,     /* reserved: collective errors (the reduction runs in the caller) */
+    IFGF_ENCCL = 5,     /* NCCL failure in the in-library all-reduce or communicator set-up
+                           (sticky like IFGF_ECUDA)                                      */
     IFGF_EINTERNAL = 6  /* invariant violation (e.g. a cousin point or parent node whose
                            cone segment is not relevant); should be impossible          */
 } ifgf_status;
@@ -62,9 +63,18 @@ typedef struct {
     double root_side;
     unsigned stage_mask;       /* IFGF_STAGE_* bits; 0 -> IFGF_STAGE_ALL                       */
     int device;                /* CUDA device ordinal; < 0 -> the current device               */
-    int rank, nranks;          /* source partition: this process owns the rank-th contiguous,
+    int rank, nranks;          /* source partition (linearity of eq. field1,
+                                  P:293-296): this process owns the rank-th contiguous,
                                   work-weighted Morton range of leaf boxes; nranks <= 1 -> all */
-    int reserved[8];           /* must be zero                                                 */
+    void* nccl_comm;           /* ncclComm_t of the nranks processes (rank = its NCCL rank),
+                                  borrowed: it must outlive the plan and is not destroyed by it
+                                  (make one with ifgf_nccl_comm_create).  Non-null: ifgf_apply
+                                  all-reduces the ranks' partial fields in place on cuda_stream,
+                                  so every rank's out is the full field.  Null: out is this
+                                  rank's partial field (the caller sums).                      */
+    int no_graph;              /* nonzero: launch the apply's kernels one by one instead of
+                                  replaying the plan's captured CUDA graph                      */
+    int reserved[7];           /* must be zero                                                 */
 } ifgf_opts;
 
 /* Fill *opts with the defaults (all zero except device = -1). */
@@ -92,11 +102,20 @@ ifgf_status ifgf_plan(const double* points, int64_t n, double k, int levels, int
  *   densities : device, 2N fp64 (complex128), caller's point order. Borrowed
  *               until the work enqueued on cuda_stream completes.
  *   out       : device, 2N fp64 (complex128), caller's order; overwritten.
- *               With nranks > 1 it holds this rank's partial field (sources of
- *               the owned leaf range only); the full field is the sum over
- *               ranks (the caller all-reduces, e.g. torch.distributed/NCCL).
+ *               With nranks > 1 and a communicator (opts.nccl_comm) it is the
+ *               full field: the ranks' partial fields (sources of each owned
+ *               leaf range) are summed by one in-place ncclAllReduce enqueued on
+ *               cuda_stream after the kernels (every rank must call ifgf_apply).
+ *               With nranks > 1 and no communicator it is this rank's partial
+ *               field.
  *   cuda_stream : cudaStream_t to enqueue on (0 = legacy default stream).
- * Asynchronous with respect to the host.
+ * Asynchronous with respect to the host.  The kernels of one apply are
+ * captured once per (densities, out) pair into a CUDA graph owned by the plan
+ * and replayed on cuda_stream (one launch instead of ~2 + 4(D-2); disabled by
+ * opts.no_graph, while ifgf_profile_enable is on, or when capture is not
+ * possible).  Errors: IFGF_EINVAL (null pointers), IFGF_ECUDA, IFGF_ENCCL
+ * (sticky), IFGF_EINTERNAL is NOT detected here (the invariant flag is read by
+ * ifgf_plan_stats and ifgf_apply_host).
  */
 ifgf_status ifgf_apply(ifgf_plan_t plan, const double* densities, double* out, void* cuda_stream);
 
@@ -107,6 +126,23 @@ ifgf_status ifgf_apply(ifgf_plan_t plan, const double* densities, double* out, v
  * but not required.
  */
 ifgf_status ifgf_apply_host(ifgf_plan_t plan, const double* densities_host, double* out_host, void* cuda_stream);
+
+/*
+ * NCCL communicator helpers (the library's own NCCL, so the communicator and
+ * the all-reduce in ifgf_apply come from one NCCL instance).
+ *   ifgf_nccl_unique_id  : id_out receives an ncclUniqueId (128 bytes, host);
+ *                          call on one rank and broadcast the bytes (e.g. with
+ *                          torch.distributed) to the others.
+ *   ifgf_nccl_comm_create: collective over the nranks processes; device is the
+ *                          CUDA ordinal this rank uses (< 0: current device);
+ *                          *comm_out receives the ncclComm_t.
+ *   ifgf_nccl_comm_destroy: releases it (after every plan using it is destroyed).
+ * Errors: IFGF_EINVAL (null pointers, rank out of range), IFGF_ENCCL.
+ */
+#define IFGF_NCCL_ID_BYTES 128
+ifgf_status ifgf_nccl_unique_id(void* id_out);
+ifgf_status ifgf_nccl_comm_create(const void* id, int nranks, int rank, int device, void** comm_out);
+ifgf_status ifgf_nccl_comm_destroy(void* comm);
 
 /* Release every device and host resource of the plan.  Null is allowed. */
 ifgf_status ifgf_plan_destroy(ifgf_plan_t plan);
@@ -133,6 +169,11 @@ typedef struct {
                                                           tensor-core GEMM, 2 per-evaluation
                                                           DFMA, 3 register-basis FP64 tensor-core
                                                           GEMM, -1 no pass (chosen at plan time) */
+    uint64_t owned_morton_begin, owned_morton_end;     /* leaf Morton keys of the owned range,
+                                                          half-open (key bit 3b+2/3b+1/3b = bit b
+                                                          of i/j/k); [0, 2^64-1) with nranks <= 1 */
+    int64_t graph_applies;                             /* applies replayed from the captured graph */
+    double partition_weight_total, partition_weight_owned; /* work-weight units (ns, model) */
 } ifgf_stats;
 
 ifgf_status ifgf_plan_stats(ifgf_plan_t plan, ifgf_stats* stats);

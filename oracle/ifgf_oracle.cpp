@@ -564,6 +564,10 @@ int build_plan(oracle_plan& p, const double* pts, int64_t n, double k, int D, in
     }
     p.H1 = H1;
     for (int a = 0; a < 3; ++a) p.x0[a] = c1[a] - H1 / 2.0;
+    if (has_root)  // B^1 must contain Gamma_N (eq. deffirstbox)
+        for (int64_t i = 0; i < n; ++i)
+            for (int a = 0; a < 3; ++a)
+                if (!(pts[3 * i + a] >= p.x0[a] && pts[3 * i + a] <= p.x0[a] + H1)) return EDOMAIN_;
 
     // Levels and cone grids.  Reading R8: (n_s, n_C)_D = (leaf_ns, leaf_nc);
     // readings R5/R6: counts double from d to d-1 iff kappa H_{d-1} > 1

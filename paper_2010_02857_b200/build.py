@@ -12,6 +12,23 @@ LIB = os.path.join(HERE, "libifgf.so")
 SOURCES = ["plan.cu", "apply.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+
+def _nccl_dir() -> str | None:
+    """The NCCL that torch loads (nvidia-nccl wheel): libifgf links the same
+    libnccl.so.2 so that one NCCL instance serves torch and the library."""
+    import site
+    for sp in site.getsitepackages() + [site.getusersitepackages()]:
+        d = os.path.join(sp, "nvidia", "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    return None
+
+
+NCCL_DIR = _nccl_dir()
+NCCL_INC = ["-I", os.path.join(NCCL_DIR, "include")] if NCCL_DIR else []
+NCCL_LINK = (["-L", os.path.join(NCCL_DIR, "lib"), "-Xlinker", "-rpath=" + os.path.join(NCCL_DIR, "lib")]
+             if NCCL_DIR else []) + ["-l:libnccl.so.2"]
+
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -19,6 +36,7 @@ NVCC_FLAGS = [
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
     "-I", os.path.join(ROOT, "include"),
+    *NCCL_INC,
 ]
 
 
@@ -43,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp, "-lcudart"]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp, "-lcudart", *NCCL_LINK]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -1324,7 +1324,8 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
                 const int sl = q < no ? sSlot[(o * UM + ui) * J + q] : -1;
                 const double2* cp = sl >= 0 ? vals_d + (int64_t)sl * P : zseg;
 #pragma unroll
-                for (int ks = 0; ks < KS; ++ks) bb[ks] = __ldg(cp + 4 * ks + tig);
+                for (int ks = 0; ks < KS; ++ks)  // k = 4 ks + tig >= P (last step): zero, not the next segment
+                    bb[ks] = 4 * ks + tig < P ? __ldg(cp + 4 * ks + tig) : make_double2(0.0, 0.0);
             };
             double2 bc[KS], bn[C::PREFETCH ? KS : 1];
             int tau = tau0;
@@ -1717,7 +1718,10 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
                 {
                     double2 b[KS];
 #pragma unroll
-                    for (int ks = 0; ks < KS; ++ks) b[ks] = __ldg(cp + (ks < 15 ? 15 * tig + ks : 60 + 4 * (ks - 15) + tig));
+                    for (int ks = 0; ks < KS; ++ks) {  // k = 60 + 4 (ks - 15) + tig >= P: zero
+                        const int kk = ks < 15 ? 15 * tig + ks : 60 + 4 * (ks - 15) + tig;
+                        b[ks] = kk < P ? __ldg(cp + kk) : make_double2(0.0, 0.0);
+                    }
 #pragma unroll
                     for (int ks = 0; ks < KS; ++ks) {
                         if (ks & 1) {

@@ -8,7 +8,15 @@
 #include <new>
 #include <string>
 
+#include <nccl.h>
+
 #include "ifgf_internal.cuh"
+
+#define IFGF_NCCL(call)                                                                              \
+    do {                                                                                             \
+        ncclResult_t r_ = (call);                                                                    \
+        if (r_ != ncclSuccess) throw ::ifgf::Error{IFGF_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
+    } while (0)
 
 namespace {
 thread_local std::string g_last_error;
@@ -24,7 +32,7 @@ ifgf_status guarded(ifgf_plan_s* p, F&& f) {
         f();
         return IFGF_OK;
     } catch (const ifgf::Error& e) {
-        if (p && e.st == IFGF_ECUDA) p->sticky_cuda_error = true;
+        if (p && (e.st == IFGF_ECUDA || e.st == IFGF_ENCCL)) p->sticky_cuda_error = true;
         return fail(e.st, e.msg);
     } catch (const std::bad_alloc&) {
         return fail(IFGF_ENOMEM, "host allocation failed");
@@ -46,6 +54,8 @@ struct DeviceGuard {
 
 void free_plan(ifgf_plan_s* p) {
     if (!p) return;
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     for (void* a : p->allocs) cudaFree(a);
     for (auto& e : p->ev_pool) cudaEventDestroy(e);
     for (auto& e : p->pending) {
@@ -53,6 +63,52 @@ void free_plan(ifgf_plan_s* p) {
         cudaEventDestroy(e.b);
     }
     delete p;
+}
+
+// One apply on stream st: the kernels replayed from the plan's CUDA
+// graph (captured on the first call for this (dens, out) pair; eager launches
+// while profiling, with opts.no_graph, or if capture is not possible), then the
+// in-place all-reduce of the ranks' partial fields when a communicator is set.
+void apply_dispatch(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t st) {
+    const bool graph = p->use_graph && !p->graph_failed && !p->profile && !p->phase_clk;
+    bool done = false;
+    if (graph) {
+        if (!p->gexec || p->g_dens != dens || p->g_out != out) {
+            if (p->gexec) {
+                IFGF_CUDA(cudaGraphExecDestroy(p->gexec));
+                p->gexec = nullptr;
+            }
+            if (!p->cap_stream) IFGF_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+            IFGF_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+            cudaGraph_t g = nullptr;
+            bool ok = true;
+            try {
+                ifgf::run_apply(p, dens, out, p->cap_stream);
+            } catch (const ifgf::Error&) {
+                ok = false;
+            }
+            cudaError_t e = cudaStreamEndCapture(p->cap_stream, &g);
+            if (ok && e == cudaSuccess && g) e = cudaGraphInstantiate(&p->gexec, g, 0);
+            else ok = false;
+            if (g) cudaGraphDestroy(g);
+            if (!ok || e != cudaSuccess) {  // not capturable here: launch eagerly from now on
+                p->gexec = nullptr;
+                p->graph_failed = true;
+                cudaGetLastError();
+            } else {
+                p->g_dens = dens;
+                p->g_out = out;
+            }
+        }
+        if (p->gexec) {
+            IFGF_CUDA(cudaGraphLaunch(p->gexec, st));
+            p->stats.graph_applies++;
+            done = true;
+        }
+    }
+    if (!done) ifgf::run_apply(p, dens, out, st);
+    if (p->nccl_comm)  // the one exchange step of the source partition
+        IFGF_NCCL(ncclAllReduce(out, out, (size_t)2 * p->n, ncclDouble, ncclSum, (ncclComm_t)p->nccl_comm, st));
 }
 
 // ------------------------------------------------------------ direct sum
@@ -242,6 +298,20 @@ ifgf_status ifgf_plan(const double* points, int64_t n, double k, int levels, int
     p->stage_mask = o.stage_mask ? o.stage_mask : IFGF_STAGE_ALL;
     p->rank = o.nranks > 1 ? o.rank : 0;
     p->nranks = o.nranks > 1 ? o.nranks : 1;
+    p->use_graph = !o.no_graph && !std::getenv("IFGF_NO_GRAPH");
+    if (o.nccl_comm) {
+        int cnt = 0, rk = 0;
+        if (ncclCommCount((ncclComm_t)o.nccl_comm, &cnt) != ncclSuccess ||
+            ncclCommUserRank((ncclComm_t)o.nccl_comm, &rk) != ncclSuccess) {
+            delete p;
+            return fail(IFGF_ENCCL, "nccl_comm is not a valid communicator");
+        }
+        if (cnt != p->nranks || rk != p->rank) {
+            delete p;
+            return fail(IFGF_EINVAL, "nccl_comm size / rank differ from nranks / rank");
+        }
+        p->nccl_comm = o.nccl_comm;
+    }
     ifgf_status st = guarded(p, [&] {
         p->dev_bad = ifgf::dev_alloc<int>(p, 1);
         IFGF_CUDA(cudaMemset(p->dev_bad, 0, sizeof(int)));
@@ -264,8 +334,8 @@ ifgf_status ifgf_apply(ifgf_plan_t p, const double* densities, double* out, void
     if (p->sticky_cuda_error) return fail(IFGF_ECUDA, "plan is in a failed CUDA state");
     DeviceGuard dg(p->device);
     return guarded(p, [&] {
-        ifgf::run_apply(p, reinterpret_cast<const double2*>(densities), reinterpret_cast<double2*>(out),
-                        (cudaStream_t)stream);
+        apply_dispatch(p, reinterpret_cast<const double2*>(densities), reinterpret_cast<double2*>(out),
+                       (cudaStream_t)stream);
     });
 }
 
@@ -280,7 +350,7 @@ ifgf_status ifgf_apply_host(ifgf_plan_t p, const double* dh, double* oh, void* s
             p->host_stage_dev_out = ifgf::dev_alloc<double2>(p, p->n);
         }
         IFGF_CUDA(cudaMemcpyAsync(p->host_stage_dev_in, dh, sizeof(double2) * p->n, cudaMemcpyHostToDevice, st));
-        ifgf::run_apply(p, p->host_stage_dev_in, p->host_stage_dev_out, st);
+        apply_dispatch(p, p->host_stage_dev_in, p->host_stage_dev_out, st);
         IFGF_CUDA(cudaMemcpyAsync(oh, p->host_stage_dev_out, sizeof(double2) * p->n, cudaMemcpyDeviceToHost, st));
         IFGF_CUDA(cudaStreamSynchronize(st));
         int bad = 0;
@@ -288,6 +358,35 @@ ifgf_status ifgf_apply_host(ifgf_plan_t p, const double* dh, double* oh, void* s
         if (bad) throw ifgf::Error{IFGF_EINTERNAL, "apply met a point outside the relevant cone segments"};
     });
     return s;
+}
+
+ifgf_status ifgf_nccl_unique_id(void* id_out) {
+    if (!id_out) return fail(IFGF_EINVAL, "null id_out");
+    static_assert(sizeof(ncclUniqueId) == IFGF_NCCL_ID_BYTES, "ncclUniqueId size");
+    return guarded(nullptr, [&] {
+        ncclUniqueId id;
+        IFGF_NCCL(ncclGetUniqueId(&id));
+        std::memcpy(id_out, &id, sizeof(id));
+    });
+}
+
+ifgf_status ifgf_nccl_comm_create(const void* id, int nranks, int rank, int device, void** comm_out) {
+    if (!id || !comm_out) return fail(IFGF_EINVAL, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(IFGF_EINVAL, "rank out of range");
+    *comm_out = nullptr;
+    DeviceGuard dg(device);
+    return guarded(nullptr, [&] {
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        ncclComm_t c = nullptr;
+        IFGF_NCCL(ncclCommInitRank(&c, nranks, uid, rank));
+        *comm_out = c;
+    });
+}
+
+ifgf_status ifgf_nccl_comm_destroy(void* comm) {
+    if (!comm) return IFGF_OK;
+    return guarded(nullptr, [&] { IFGF_NCCL(ncclCommDestroy((ncclComm_t)comm)); });
 }
 
 ifgf_status ifgf_plan_destroy(ifgf_plan_t p) {

@@ -169,6 +169,16 @@ struct ifgf_plan_s {
     unsigned long long* phase_clk = nullptr;  // env IFGF_PHASE_PROF: TC K7 per-phase clock sums
     int64_t device_bytes = 0;
     std::vector<void*> allocs;  // every cudaMalloc of the plan
+    // multi-GPU: borrowed ncclComm_t (opts.nccl_comm); ifgf_apply all-reduces out
+    void* nccl_comm = nullptr;
+    // CUDA graph of one apply (captured on cap_stream for one (densities, out) pair,
+    // replayed on the caller's stream)
+    bool use_graph = true;
+    bool graph_failed = false;
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    const void* g_dens = nullptr;
+    void* g_out = nullptr;
 };
 
 namespace ifgf {

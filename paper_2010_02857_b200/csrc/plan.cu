@@ -213,6 +213,28 @@ __global__ void k_cousins(const int* __restrict__ ijk, const int* __restrict__ p
     if (!pass) cnt[b] = c;
 }
 
+// Partition work units per box: near-field pairs of a leaf as
+// source (its points times the points of its neighbour leaves, minus the self
+// pairs) and cousin evaluations of a box as source (the points of its cousins).
+__global__ void k_box_units(const int* __restrict__ start, const int* __restrict__ nbr_off,
+                            const int* __restrict__ nbr_idx, const int* __restrict__ cou_off,
+                            const int* __restrict__ cou_idx, int64_t nb, double* near_units, double* cou_units) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const double nbx = (double)(start[b + 1] - start[b]);
+    if (near_units) {
+        int64_t s = 0;
+        for (int e = nbr_off[b]; e < nbr_off[b + 1]; ++e) s += start[nbr_idx[e] + 1] - start[nbr_idx[e]];
+        near_units[b] = nbx * (double)s - nbx;
+    }
+    if (cou_units) {
+        int64_t s = 0;
+        if (cou_off)
+            for (int e = cou_off[b]; e < cou_off[b + 1]; ++e) s += start[cou_idx[e] + 1] - start[cou_idx[e]];
+        cou_units[b] = (double)s;
+    }
+}
+
 // Warp work items: (box, first point) chunks of 32 points.
 __global__ void k_witem_count(const int* __restrict__ start, int64_t nb, int* cnt) {
     int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -652,6 +674,10 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         t_mark = t;
     };
 
+    // The plan works on its own non-blocking stream: finish every piece of work
+    // already enqueued on the device (e.g. the caller's copy into `points`) first.
+    IFGF_CUDA(cudaDeviceSynchronize());
+
     // 1. validation + bounding box
     {
         int nb = 148 * 4;
@@ -687,6 +713,13 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             p->H1 = (1.0 + std::ldexp(1.0, -20)) * ext;
         }
         for (int a = 0; a < 3; ++a) p->x0[a] = p->root_c[a] - p->H1 / 2.0;
+        // A caller-supplied root box must contain Gamma_N (eq. deffirstbox);
+        // points outside it would be clamped into boundary leaves and the cousin
+        // separation the interpolation relies on would not hold.
+        if (o.has_root)
+            for (int a = 0; a < 3; ++a)
+                if (!(lo[a] >= p->x0[a] && hi[a] <= p->x0[a] + p->H1))
+                    throw Error{IFGF_EDOMAIN, "the root box does not contain every point"};
     }
 
     step_time("1 validation+bbox");
@@ -915,25 +948,76 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         LevelHost& LD = p->lev[D];
         int64_t nleaf = LD.p.nbox;
         int64_t L0 = 0, L1 = nleaf;
+        p->stats.partition_weight_total = p->stats.partition_weight_owned = 0.0;
         if (p->nranks > 1) {
-            // work weight per leaf: points^2 (near + s2c proxy) + points * levels (cousin proxy)
-            std::vector<int> starts(nleaf + 1);
-            IFGF_CUDA(cudaMemcpy(starts.data(), LD.box_start, sizeof(int) * (nleaf + 1), cudaMemcpyDeviceToHost));
-            // work weight per leaf (ns on one B200, cfg4 per-unit costs):
-            // near field ~0.1 m^2 (m targets x ~14 neighbour leaves of similar size),
-            // source-to-cone + cousins ~(3.2 + 2.3 (D - 2)) m, and the upward passes of
-            // its ancestors ~100 (D - 2) per leaf independent of m (per-box cone data)
+            // Work weight per leaf L, in ps on one B200:
+            //   w(L) = c3 near(L) + c4 s2c(L) + n_L sum_{A ancestor of L, d >= 3} (c6 + rho c7) cou(A) / n_A
+            // with the plan's unit counts: near(L) = near-field pairs with L as source,
+            // s2c(L) = n_L |cells_D| P (source-to-cone pairs; every leaf cell is relevant
+            // at the default grid), cou(A) = cousin evaluations with A as source; the
+            // upward evaluations of A (known only after the relevance pass) are proxied
+            // by rho cou(A), rho = 2.7 = sum upward / sum cousin evaluations at cfg4; A's
+            // work is apportioned to its leaves by their points.  c3 = 6.0, c4 = 4.7,
+            // c6 = 41, c7 = 32 ps per unit: the measured cfg4 kernel time per unit
+            // (r01m: 48 ms / 8.0e9, 71 ms / 1.5e10, 384 ms / 9.3e9, 805 ms / 2.5e10).
+            const double c3 = 6.0, c4 = 4.7, c6 = 41.0, c7 = 32.0, rho = 2.7;
+            std::vector<std::vector<int>> start(D + 1), parent(D + 1);
+            std::vector<std::vector<double>> cou(D + 1);
+            std::vector<double> near(nleaf);
+            for (int d = 3; d <= D; ++d) {
+                LevelHost& L = p->lev[d];
+                const int64_t nb = L.p.nbox;
+                double* dnear = d == D ? S.get<double>(nb) : nullptr;
+                double* dcou = S.get<double>(nb);
+                k_box_units<<<nblocks(nb), TPB, 0, st>>>(L.box_start, L.nbr_off, L.nbr_idx, L.cou_off, L.cou_idx, nb,
+                                                         dnear, dcou);
+                IFGF_CUDA(cudaGetLastError());
+                start[d].resize(nb + 1);
+                cou[d].resize(nb);
+                parent[d].resize(nb);
+                IFGF_CUDA(cudaMemcpyAsync(start[d].data(), L.box_start, sizeof(int) * (nb + 1), cudaMemcpyDeviceToHost, st));
+                IFGF_CUDA(cudaMemcpyAsync(cou[d].data(), dcou, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+                IFGF_CUDA(cudaMemcpyAsync(parent[d].data(), L.box_parent, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
+                if (dnear)
+                    IFGF_CUDA(cudaMemcpyAsync(near.data(), dnear, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+                IFGF_CUDA(cudaStreamSynchronize(st));
+                if (dnear) S.release(dnear);
+                S.release(dcou);
+            }
             std::vector<double> w(nleaf);
+            const double cells_D = (double)LD.p.ncell;
             for (int64_t b = 0; b < nleaf; ++b) {
-                const double m = starts[b + 1] - starts[b];
-                w[b] = 0.1 * m * m + (3.2 + 2.3 * (D - 2)) * m * (P / 75.0) + 100.0 * (D - 2) * (P / 75.0);
+                const double m = start[D][b + 1] - start[D][b];
+                double anc = 0.0;
+                for (int64_t a = b, d = D; d >= 3; --d) {
+                    const double na = start[d][a + 1] - start[d][a];
+                    anc += (c6 + rho * c7) * cou[d][a] / std::max(1.0, na);
+                    a = parent[d][a];
+                }
+                w[b] = c3 * near[b] + c4 * cells_D * P * m + m * anc;
             }
             std::vector<int64_t> bounds(p->nranks + 1);
             ifgf_status ps = ifgf_partition(w.data(), nleaf, p->nranks, bounds.data());
             if (ps != IFGF_OK) throw Error{ps, "partition failed"};
             L0 = bounds[p->rank];
             L1 = bounds[p->rank + 1];
+            for (int64_t b = 0; b < nleaf; ++b) {
+                p->stats.partition_weight_total += w[b];
+                if (b >= L0 && b < L1) p->stats.partition_weight_owned += w[b];
+            }
         }
+        // owned range as leaf Morton keys (half-open; the end is the first leaf of the next rank)
+        auto leaf_key = [&](int64_t b) -> uint64_t {
+            int ijk[3];
+            IFGF_CUDA(cudaMemcpy(ijk, LD.box_ijk + 3 * b, sizeof(ijk), cudaMemcpyDeviceToHost));
+            uint64_t r = 0;
+            for (int bit = 0; bit < 21; ++bit)
+                r |= ((uint64_t)((ijk[0] >> bit) & 1) << (3 * bit + 2)) | ((uint64_t)((ijk[1] >> bit) & 1) << (3 * bit + 1)) |
+                     ((uint64_t)((ijk[2] >> bit) & 1) << (3 * bit));
+            return r;
+        };
+        p->stats.owned_morton_begin = L0 == 0 ? 0 : (L0 < nleaf ? leaf_key(L0) : ~(uint64_t)0);
+        p->stats.owned_morton_end = L1 >= nleaf ? ~(uint64_t)0 : leaf_key(L1);
         p->stats.owned_leaf_begin = L0;
         p->stats.owned_leaf_end = L1;
         int64_t a = L0, b = L1 - 1;  // inclusive leaf range (may be empty)

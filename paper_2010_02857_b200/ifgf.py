@@ -1,8 +1,10 @@
 """Thin ctypes binding of libifgf.so (include/ifgf.h).
 
 Argument marshalling only: every step of the IFGF path runs in the library's
-CUDA kernels.  PyTorch supplies device memory, streams and (for multi-GPU)
-``torch.distributed``; there is no CPU fallback -- importing this module on a
+CUDA kernels.  PyTorch supplies device memory, streams and (for multi-GPU) the
+``torch.distributed`` broadcast of the NCCL unique id; the all-reduce of the
+ranks' partial fields runs inside ``ifgf_apply`` on a communicator the library
+creates (``NcclComm``).  There is no CPU fallback -- importing this module on a
 box without the built library raises.
 """
 from __future__ import annotations
@@ -33,7 +35,8 @@ class IfgfOpts(ctypes.Structure):
         ("has_root", ctypes.c_int), ("root_center", ctypes.c_double * 3), ("root_side", ctypes.c_double),
         ("stage_mask", ctypes.c_uint), ("device", ctypes.c_int),
         ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
-        ("reserved", ctypes.c_int * 8),
+        ("nccl_comm", ctypes.c_void_p), ("no_graph", ctypes.c_int),
+        ("reserved", ctypes.c_int * 7),
     ]
 
 
@@ -53,6 +56,9 @@ class IfgfStats(ctypes.Structure):
         ("segment_bytes", ctypes.c_int64 * _L1),
         ("plan_device_bytes", ctypes.c_int64), ("plan_ms", ctypes.c_double),
         ("upward_kernel", ctypes.c_int * _L1),
+        ("owned_morton_begin", ctypes.c_uint64), ("owned_morton_end", ctypes.c_uint64),
+        ("graph_applies", ctypes.c_int64),
+        ("partition_weight_total", ctypes.c_double), ("partition_weight_owned", ctypes.c_double),
     ]
 
 
@@ -74,6 +80,9 @@ _SIGS = {
     "ifgf_status_string": ([_c_i], ctypes.c_char_p),
     "ifgf_last_error_message": ([], ctypes.c_char_p),
     "ifgf_version": ([], ctypes.c_char_p),
+    "ifgf_nccl_unique_id": ([_c_p], _c_i),
+    "ifgf_nccl_comm_create": ([_c_p, _c_i, _c_i, _c_i, ctypes.POINTER(_c_p)], _c_i),
+    "ifgf_nccl_comm_destroy": ([_c_p], _c_i),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -116,23 +125,76 @@ def _c128_cuda(x: torch.Tensor, name: str) -> torch.Tensor:
     return x.contiguous()
 
 
+class NcclComm:
+    """An NCCL communicator created by the library (ifgf_nccl_comm_create) from a
+    unique id that rank 0 draws and ``torch.distributed`` broadcasts; passed to
+    ``Plan(comm=...)`` it makes ``apply`` return the full field on every rank
+    (in-library ncclAllReduce of the partial fields)."""
+
+    ID_BYTES = 128
+
+    def __init__(self, nranks: int, rank: int, device: int, unique_id: bytes):
+        if len(unique_id) != self.ID_BYTES:
+            raise ValueError("unique_id must be 128 bytes")
+        self.nranks, self.rank, self.device = int(nranks), int(rank), int(device)
+        buf = ctypes.create_string_buffer(bytes(unique_id), self.ID_BYTES)
+        h = ctypes.c_void_p()
+        _check(_lib.ifgf_nccl_comm_create(buf, self.nranks, self.rank, self.device, ctypes.byref(h)),
+               "ifgf_nccl_comm_create")
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(NcclComm.ID_BYTES)
+        _check(_lib.ifgf_nccl_unique_id(buf), "ifgf_nccl_unique_id")
+        return buf.raw
+
+    @classmethod
+    def from_group(cls, group=None, device: int | None = None) -> "NcclComm":
+        """Collective over a torch.distributed group (any backend): rank 0's unique
+        id is broadcast with broadcast_object_list."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        dev = torch.cuda.current_device() if device is None else int(device)
+        return cls(world, rank, dev, obj[0])
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.ifgf_nccl_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Plan:
     """IFGF plan: ``ifgf_plan(points, k, levels, P_s, P_ang)`` (C ABI).
 
     points: float64 [N, 3] CUDA tensor.  ``rank``/``nranks`` select this
-    process's source partition (``apply`` then returns the partial field and,
-    if ``group`` is given, all-reduces it with torch.distributed).
+    process's source partition; with ``comm`` (an ``NcclComm`` of the nranks
+    processes) ``apply`` returns the full field on every rank, without it this
+    rank's partial field.  ``graph=False`` launches the kernels one by one
+    instead of replaying the plan's CUDA graph.
     """
 
     def __init__(self, points: torch.Tensor, k: float, levels: int, P_s: int = 3, P_ang: int = 5, *,
                  leaf_ns: int = 0, leaf_nc: int = 0, root=None, stage_mask: int = 0, rank: int = 0,
-                 nranks: int = 1, group=None):
+                 nranks: int = 1, comm: NcclComm | None = None, graph: bool = True):
         pts = _f64_cuda(points, "points")
         if pts.dim() != 2 or pts.shape[1] != 3:
             raise ValueError("points must be [N, 3]")
         self.n = int(pts.shape[0])
         self.device = pts.device
-        self.group = group
+        self.comm = comm  # borrowed by the library plan: keep it alive as long as the plan
         o = IfgfOpts()
         _check(_lib.ifgf_opts_init(ctypes.byref(o)), "ifgf_opts_init")
         o.leaf_ns, o.leaf_nc = int(leaf_ns), int(leaf_nc)
@@ -144,8 +206,9 @@ class Plan:
         o.stage_mask = int(stage_mask)
         o.device = pts.device.index if pts.device.index is not None else torch.cuda.current_device()
         o.rank, o.nranks = int(rank), int(nranks)
+        o.nccl_comm = comm.handle.value if comm is not None else None
+        o.no_graph = 0 if graph else 1
         h = ctypes.c_void_p()
-        torch.cuda.synchronize(pts.device)
         _check(_lib.ifgf_plan(pts.data_ptr(), self.n, float(k), int(levels), int(P_s), int(P_ang), ctypes.byref(o),
                               ctypes.byref(h)), "ifgf_plan")
         self._h = h
@@ -166,33 +229,51 @@ class Plan:
         except Exception:
             pass
 
+    def _check_dev(self, x: torch.Tensor, name: str):
+        if x.device != self.device:
+            raise ValueError(f"{name} is on {x.device}, the plan on {self.device}")
+
     def apply(self, a: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        """out = I(a) (complex128 [N] CUDA tensors, caller's point order)."""
+        """out = I(a) (complex128 [N] CUDA tensors on the plan's device, caller's
+        point order), enqueued on ``stream`` (default: the current stream)."""
         a = _c128_cuda(a, "densities")
+        self._check_dev(a, "densities")
         if a.shape != (self.n,):
             raise ValueError("densities must be [N]")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
         if out is None:
-            out = torch.empty(self.n, dtype=torch.complex128, device=a.device)
+            with torch.cuda.stream(s):
+                out = torch.empty(self.n, dtype=torch.complex128, device=self.device)
         elif not out.is_contiguous() or out.dtype != torch.complex128 or out.shape != (self.n,):
             raise ValueError("out must be a contiguous complex128 [N] tensor")
-        _check(_lib.ifgf_apply(self._h, a.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "ifgf_apply")
-        if self.group is not None:
-            allreduce_field(out, self.group)
+        self._check_dev(out, "out")
+        if s != torch.cuda.current_stream(self.device):
+            a.record_stream(s)  # the contiguous copy (if any) lives until the library's work on s is done
+            out.record_stream(s)
+        _check(_lib.ifgf_apply(self._h, a.data_ptr(), out.data_ptr(), s.cuda_stream), "ifgf_apply")
         return out
 
     def apply_host(self, a_host: np.ndarray | torch.Tensor, out_host=None, stream=None):
-        """End-to-end apply from host buffers (ifgf_apply_host): H2D, apply, D2H, sync."""
-        if isinstance(a_host, torch.Tensor):
-            a = a_host.contiguous()
-            assert a.dtype == torch.complex128 and not a.is_cuda
-            ptr = a.data_ptr()
-        else:
-            a = np.ascontiguousarray(a_host, dtype=np.complex128)
-            ptr = a.ctypes.data
+        """End-to-end apply from host buffers (ifgf_apply_host): H2D, apply, D2H, sync.
+        a_host / out_host: complex128 [N] host arrays (numpy or CPU tensors; pinned
+        memory is faster)."""
+        def host_buf(x, name):
+            if isinstance(x, torch.Tensor):
+                if x.is_cuda or x.dtype != torch.complex128 or x.shape != (self.n,) or not x.is_contiguous():
+                    raise ValueError(f"{name} must be a contiguous complex128 [N] host tensor")
+                return x, x.data_ptr()
+            x = np.asarray(x)
+            if x.dtype != np.complex128 or x.shape != (self.n,) or not x.flags.c_contiguous:
+                raise ValueError(f"{name} must be a contiguous complex128 [N] array")
+            return x, x.ctypes.data
+        a, ptr = host_buf(a_host, "densities")
         if out_host is None:
             out_host = torch.empty(self.n, dtype=torch.complex128, pin_memory=True)
-        optr = out_host.data_ptr() if isinstance(out_host, torch.Tensor) else out_host.ctypes.data
-        _check(_lib.ifgf_apply_host(self._h, ptr, optr, _stream_ptr(stream)), "ifgf_apply_host")
+        if isinstance(out_host, np.ndarray) and not out_host.flags.writeable:
+            raise ValueError("out must be writeable")
+        out_host, optr = host_buf(out_host, "out")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(_lib.ifgf_apply_host(self._h, ptr, optr, s.cuda_stream), "ifgf_apply_host")
         return out_host
 
     def stats(self) -> dict:
@@ -204,6 +285,7 @@ class Plan:
             n=s.n, levels=D, P_s=s.P_s, P_ang=s.P_ang, P=s.P, k=s.k,
             root_center=list(s.root_center), root_side=s.root_side,
             owned_leaf_range=(s.owned_leaf_begin, s.owned_leaf_end),
+            owned_morton_range=(s.owned_morton_begin, s.owned_morton_end),
             nbox={d: s.nbox[d] for d in lv}, nseg={d: s.nseg[d] for d in lv},
             grid={d: (s.ns[d], s.nC[d]) for d in lv},
             near_pairs=s.near_pairs, s2c_pairs=s.s2c_pairs,
@@ -211,6 +293,8 @@ class Plan:
             segment_bytes={d: s.segment_bytes[d] for d in lv},
             plan_device_bytes=s.plan_device_bytes, plan_ms=s.plan_ms,
             upward_kernel={d: s.upward_kernel[d] for d in lv},
+            graph_applies=s.graph_applies,
+            partition_weight=(s.partition_weight_owned, s.partition_weight_total),
         )
 
     def level_segments(self, d: int) -> np.ndarray:
@@ -231,14 +315,6 @@ class Plan:
         _check(_lib.ifgf_profile_read(self._h, ms.ctypes.data, ln.ctypes.data, 1 if reset else 0),
                "ifgf_profile_read")
         return {KCLASS_NAMES[c]: (float(ms[c]), int(ln[c])) for c in range(NUM_KCLASS)}
-
-
-def allreduce_field(field: torch.Tensor, group=None) -> torch.Tensor:
-    """Sum the ranks' partial fields in place (the one exchange step of the
-    source-partitioned matvec; NCCL over NVLink on GPUs, gloo in CPU tests)."""
-    import torch.distributed as dist
-    dist.all_reduce(torch.view_as_real(field), op=dist.ReduceOp.SUM, group=group)
-    return field
 
 
 def direct(points: torch.Tensor, k: float, a: torch.Tensor, targets: torch.Tensor, stream=None) -> torch.Tensor:

@@ -23,3 +23,13 @@ def test_workload_config_names_every_config():
         assert cfg["N"] == c.n and cfg["levels"] == c.levels and cfg["parallelism"] == "1 GPU"
         assert math.isclose(cfg["k"], c.k)
     assert "x8" in bench.workload_config(inputs.CONFIGS["cfg4"], 8)["parallelism"]
+
+
+def test_oracle_sample_slice():
+    """The bounded CPU sample (cpu_baseline / --impl reference): a Morton slice of
+    the leaves, its partial apply, and the rate extrapolated by its share of sources."""
+    smp = bench.OracleSample(inputs.CONFIGS["cfg2"])
+    assert 0.0 < smp.frac < 0.02
+    t = smp.step()
+    assert t > 0 and smp.value(t) == smp.frac * smp.c.n / t
+    assert "Morton slice" in smp.desc and smp.cores >= 1

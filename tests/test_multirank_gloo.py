@@ -1,7 +1,10 @@
 """World-size-2 (and 3) CPU test of the multi-GPU host logic over gloo: the
-work-weighted Morton partition (ifgf_partition, host-only), the per-rank
-source restriction (exact by linearity of eq. field1) and the all-reduce helper
-the GPU path uses (ifgf.allreduce_field).  Partial fields come from the oracle."""
+contiguous weighted Morton partition (ifgf_partition, host-only), the per-rank
+source restriction (exact by linearity of eq. field1)
+and the one exchange step, a sum of the ranks' partial fields over all N targets
+(in the product an in-library ncclAllReduce; here a gloo all_reduce of the same
+arrays).  Partial fields come from oracle plans that own each rank's Morton
+range of leaves."""
 import math
 import os
 import socket
@@ -43,17 +46,21 @@ def _worker(rank, world, port, n, D, result_q):
     a = inputs.densities(n)
     plan = oracle.OraclePlan(pts, k, D, 3, 5)
     leaves = plan.level_boxes(D)
-    order = np.argsort([morton3(*b[:3]) for b in leaves], kind="stable")
-    counts = leaves[order, 3].astype(np.float64)
-    w = 14.0 * counts ** 2 + 8.0 * 75 * counts + 180.0 * (D - 2) * counts
+    keys = np.array([morton3(*b[:3]) for b in leaves], dtype=np.uint64)
+    order = np.argsort(keys, kind="stable")
+    w = leaves[order, 3].astype(np.float64)  # any non-negative weights: points per leaf
     bounds = ifgf.partition(w, world)
-    owned = {tuple(leaves[order[i], :3]) for i in range(bounds[rank], bounds[rank + 1])}
+    lo = int(keys[order[bounds[rank]]]) if bounds[rank] < len(keys) else 2 ** 64 - 1
+    hi = int(keys[order[bounds[rank + 1]]]) if bounds[rank + 1] < len(keys) else 2 ** 64 - 1
+    if bounds[rank] == 0:
+        lo = 0
+    part = oracle.OraclePlan(pts, k, D, 3, 5, owned_morton=(lo, hi)).apply(a)
     info = plan.level_info(D)
     q = np.clip(np.floor((pts - info["x0"]) / info["H"]).astype(np.int64), 0, 2 ** (D - 1) - 1)
-    mine = np.array([tuple(x) in owned for x in q])
-    part = plan.apply(np.where(mine, a, 0.0))
+    qk = np.array([morton3(*x) for x in q], dtype=np.uint64)
+    mine = (qk >= np.uint64(lo)) & (qk < np.uint64(hi))
     field = torch.from_numpy(part.copy())
-    ifgf.allreduce_field(field)
+    dist.all_reduce(torch.view_as_real(field), op=dist.ReduceOp.SUM)
     full = plan.apply(a)
     cover = torch.tensor([int(mine.sum())])
     dist.all_reduce(cover)
