@@ -144,6 +144,26 @@ ifgf_status ifgf_nccl_unique_id(void* id_out);
 ifgf_status ifgf_nccl_comm_create(const void* id, int nranks, int rank, int device, void** comm_out);
 ifgf_status ifgf_nccl_comm_destroy(void* comm);
 
+/*
+ * Test hook: one level's steps in isolation on caller-supplied node values
+ * (SURVEY.md §8(c) exact pin 2, polynomial injection; Algorithm 1).
+ *   d      : level, 3 <= d <= levels.
+ *   values : host, nseg_d x P complex128 node values of level d's relevant
+ *            segments in the order of ifgf_plan_level_segments, nodes s-fastest
+ *            ((c P_ang + b) P_s + a for the a-th s, b-th theta, c-th phi
+ *            first-kind Chebyshev node).  They replace the level's values and
+ *            are fitted to Chebyshev coefficients (K5).
+ *   what   : bit 0 -> K6 of level d alone: field (host, 2N fp64, caller order)
+ *            = sum over (target, cousin box) pairs of Interp(x) G(x, c_B);
+ *            bit 1 -> K7 d -> d-1 (d > 3): parent (host, nseg_{d-1} x P
+ *            complex128) = level d-1's Chebyshev coefficients after the
+ *            upward pass from these values alone (plus its fit).
+ * Synchronous.  Overwrites the plan's apply scratch (not thread-safe with a
+ * concurrent apply).  Errors: IFGF_EINVAL, IFGF_ECUDA.
+ */
+ifgf_status ifgf_debug_level_pass(ifgf_plan_t plan, int d, const double* values, unsigned what, double* field,
+                                  double* parent);
+
 /* Release every device and host resource of the plan.  Null is allowed. */
 ifgf_status ifgf_plan_destroy(ifgf_plan_t plan);
 

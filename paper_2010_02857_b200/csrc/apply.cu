@@ -1888,6 +1888,61 @@ struct Prof {  // CUDA events around each launch (ifgf_profile_enable)
 
 }  // namespace
 
+// K5 fit of level d's node values into Chebyshev coefficients, in place.
+void fit_level(ifgf_plan_s* p, int d, cudaStream_t st) {
+    const int P = p->P, Ps = p->Ps, Pa = p->Pa;
+    LevelParams& L = p->lev[d].p;
+    if (L.nseg == 0) return;
+    const int fit_warps = std::max(1, std::min(4, (int)(48 * 1024 / (32 * P))));
+    const size_t fit_smem = (size_t)fit_warps * 2 * P * sizeof(double2);
+    if (fit_smem > 48 * 1024)
+        IFGF_CUDA(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fit_smem));
+    Prof pr(p, st, 3);
+    const unsigned nb8 = (unsigned)((L.nseg + 3) / 4);
+    dispatch(
+        Ps, Pa, [&] { k_fit_lines<3, 5><<<nb8, 64, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
+        [&] { k_fit_lines<5, 5><<<nb8, 64, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
+        [&] {
+            k_fit<<<(int)((L.nseg + fit_warps - 1) / fit_warps), 32 * fit_warps, fit_smem, st>>>(
+                L.nseg, Ps, Pa, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]);
+        });
+    pr.done();
+}
+
+// K6 of level d: out_sorted += cousin interpolation (Morton order).
+void cousin_level(ifgf_plan_s* p, int d, cudaStream_t st) {
+    LevelParams& L = p->lev[d].p;
+    if (L.nseg == 0 || L.nwitems == 0) return;
+    Prof pr(p, st, 4);
+    const double2* vd = p->vals[d & 1];
+    dim3 g(nblk(L.nwitems * 32));
+    dispatch(
+        p->Ps, p->Pa, [&] { Kern<3, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
+        [&] { Kern<5, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
+        [&] { Kern<0, 0>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); });
+    pr.done();
+}
+
+// K7 d -> d-1 (+ the K5 fit of level d-1 when the kernel does not fuse it).
+void upward_level(ifgf_plan_s* p, int d, cudaStream_t st) {
+    LevelParams& L = p->lev[d].p;
+    LevelParams& LP = p->lev[d - 1].p;
+    if (LP.nseg == 0) return;
+    bool fused = false;
+    {
+        Prof pr(p, st, 5);
+        dim3 g(nblk(LP.nseg * p->P));
+        const double2* vd = p->vals[d & 1];
+        double2* vp = p->vals[(d - 1) & 1];
+        dispatch(
+            p->Ps, p->Pa, [&] { fused = Kern<3, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
+            [&] { fused = Kern<5, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
+            [&] { fused = Kern<0, 0>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); });
+        pr.done();
+    }
+    if (!fused) fit_level(p, d - 1, st);
+}
+
 void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t st) {
     const int D = p->D, P = p->P, Ps = p->Ps, Pa = p->Pa;
     const int64_t n = p->n;
@@ -1930,24 +1985,6 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
         }
         have = true;
     }
-    const int fit_warps = std::max(1, std::min(4, (int)(48 * 1024 / (32 * P))));
-    const size_t fit_smem = (size_t)fit_warps * 2 * P * sizeof(double2);
-    if (fit_smem > 48 * 1024)
-        IFGF_CUDA(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fit_smem));
-    auto fit = [&](int d) {
-        LevelParams& L = p->lev[d].p;
-        if (L.nseg == 0) return;
-        Prof pr(p, st, 3);
-        const unsigned nb8 = (unsigned)((L.nseg + 3) / 4);
-        dispatch(
-            Ps, Pa, [&] { k_fit_lines<3, 5><<<nb8, 64, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
-            [&] { k_fit_lines<5, 5><<<nb8, 64, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
-            [&] {
-                k_fit<<<(int)((L.nseg + fit_warps - 1) / fit_warps), 32 * fit_warps, fit_smem, st>>>(
-                    L.nseg, Ps, Pa, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]);
-            });
-        pr.done();
-    };
     auto phase_dump = [&](int dl) {
         if (!p->phase_clk) return;
         unsigned long long h[16];
@@ -1965,34 +2002,12 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
                 (double)h[10] / std::max(1.0, (double)h[12]), (double)h[11] / std::max(1.0, (double)h[12]),
                 (double)h[12] / std::max(1.0, (double)h[13]));
     };
-    if (have && !leaf_fused) fit(D);
+    if (have && !leaf_fused) fit_level(p, D, st);
     for (int d = D; d >= 3 && have; --d) {
-        LevelParams& L = p->lev[d].p;
-        const double2* vd = p->vals[d & 1];
-        if ((mask & IFGF_STAGE_COUSIN) && L.nseg > 0 && L.nwitems > 0) {
-            Prof pr(p, st, 4);
-            dim3 g(nblk(L.nwitems * 32));
-            dispatch(
-                Ps, Pa, [&] { Kern<3, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
-                [&] { Kern<5, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
-                [&] { Kern<0, 0>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); });
-            pr.done();
-        }
+        if (mask & IFGF_STAGE_COUSIN) cousin_level(p, d, st);
         if (d > 3 && (mask & IFGF_STAGE_UPWARD)) {
-            LevelParams& LP = p->lev[d - 1].p;
-            if (LP.nseg > 0) {
-                Prof pr(p, st, 5);
-                dim3 g(nblk(LP.nseg * P));
-                double2* vp = p->vals[(d - 1) & 1];
-                bool fused = false;
-                dispatch(
-                    Ps, Pa, [&] { fused = Kern<3, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
-                    [&] { fused = Kern<5, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
-                    [&] { fused = Kern<0, 0>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); });
-                pr.done();
-                phase_dump(d - 1);
-                if (!fused) fit(d - 1);
-            }
+            upward_level(p, d, st);
+            phase_dump(d - 1);
         } else {
             have = false;
         }
@@ -2002,6 +2017,38 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
         k_unpermute<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->perm, n, out);
         pr.done();
     }
+}
+
+// Test hook (ifgf_debug_level_pass): one level's K5 / K6 / K7 in isolation on
+// caller-supplied node values (SURVEY.md §8(c) exact pin 2, polynomial injection).
+void debug_level_pass(ifgf_plan_s* p, int d, const double2* values_h, unsigned what, double2* field_h,
+                      double2* parent_h) {
+    const int P = p->P;
+    const int64_t n = p->n;
+    cudaStream_t st;
+    IFGF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    } sg{st};
+    LevelParams& L = p->lev[d].p;
+    IFGF_CUDA(cudaMemcpyAsync(p->vals[d & 1], values_h, sizeof(double2) * (size_t)L.nseg * P, cudaMemcpyHostToDevice, st));
+    fit_level(p, d, st);
+    if (what & 1) {
+        IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));
+        cousin_level(p, d, st);
+        double2* tmp = nullptr;
+        IFGF_CUDA(cudaMallocAsync((void**)&tmp, sizeof(double2) * n, st));
+        k_unpermute<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->perm, n, tmp);
+        IFGF_CUDA(cudaMemcpyAsync(field_h, tmp, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
+        IFGF_CUDA(cudaFreeAsync(tmp, st));
+    }
+    if ((what & 2) && d > 3) {
+        upward_level(p, d, st);
+        IFGF_CUDA(cudaMemcpyAsync(parent_h, p->vals[(d - 1) & 1], sizeof(double2) * (size_t)p->lev[d - 1].p.nseg * P,
+                                  cudaMemcpyDeviceToHost, st));
+    }
+    IFGF_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace ifgf

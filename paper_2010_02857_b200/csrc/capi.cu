@@ -360,6 +360,20 @@ ifgf_status ifgf_apply_host(ifgf_plan_t p, const double* dh, double* oh, void* s
     return s;
 }
 
+ifgf_status ifgf_debug_level_pass(ifgf_plan_t p, int d, const double* values, unsigned what, double* field,
+                                  double* parent) {
+    if (!p || !values) return fail(IFGF_EINVAL, "null argument");
+    if (d < 3 || d > p->D) return fail(IFGF_EINVAL, "level must be in [3, levels]");
+    if ((what & 1) && !field) return fail(IFGF_EINVAL, "null field");
+    if ((what & 2) && d > 3 && !parent) return fail(IFGF_EINVAL, "null parent");
+    if (p->sticky_cuda_error) return fail(IFGF_ECUDA, "plan is in a failed CUDA state");
+    DeviceGuard dg(p->device);
+    return guarded(p, [&] {
+        ifgf::debug_level_pass(p, d, reinterpret_cast<const double2*>(values), what, reinterpret_cast<double2*>(field),
+                               reinterpret_cast<double2*>(parent));
+    });
+}
+
 ifgf_status ifgf_nccl_unique_id(void* id_out) {
     if (!id_out) return fail(IFGF_EINVAL, "null id_out");
     static_assert(sizeof(ncclUniqueId) == IFGF_NCCL_ID_BYTES, "ncclUniqueId size");

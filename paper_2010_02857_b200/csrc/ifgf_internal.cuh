@@ -197,6 +197,8 @@ void dev_free(ifgf_plan_s* p, void* ptr);
 
 void build_plan(ifgf_plan_s* p, const double* points_dev, const ifgf_opts& o);
 void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t st);
+void debug_level_pass(ifgf_plan_s* p, int d, const double2* values_h, unsigned what, double2* field_h,
+                      double2* parent_h);
 
 // ---------------------------------------------------------------------------
 // Device helpers

@@ -80,6 +80,7 @@ _SIGS = {
     "ifgf_status_string": ([_c_i], ctypes.c_char_p),
     "ifgf_last_error_message": ([], ctypes.c_char_p),
     "ifgf_version": ([], ctypes.c_char_p),
+    "ifgf_debug_level_pass": ([_c_p, _c_i, _c_p, ctypes.c_uint, _c_p, _c_p], _c_i),
     "ifgf_nccl_unique_id": ([_c_p], _c_i),
     "ifgf_nccl_comm_create": ([_c_p, _c_i, _c_i, _c_i, ctypes.POINTER(_c_p)], _c_i),
     "ifgf_nccl_comm_destroy": ([_c_p], _c_i),
@@ -305,6 +306,23 @@ class Plan:
             _check(_lib.ifgf_plan_level_segments(self._h, d, out.ctypes.data, cnt.value, ctypes.byref(cnt)),
                    "ifgf_plan_level_segments")
         return out
+
+    def debug_level_pass(self, d: int, values: np.ndarray, cousin: bool = True, upward: bool = True):
+        """Test hook (ifgf_debug_level_pass): K5 + K6 and/or K7 of level d alone on
+        the given node values (complex128 [nseg_d, P], plan segment order).
+        Returns (field [N] or None, parent coefficients [nseg_{d-1}, P] or None)."""
+        st = self.stats()
+        v = np.ascontiguousarray(values, dtype=np.complex128)
+        if v.shape != (st["nseg"][d], st["P"]):
+            raise ValueError("values must be [nseg_d, P]")
+        what = (1 if cousin else 0) | (2 if upward and d > 3 else 0)
+        field = np.zeros(self.n, dtype=np.complex128) if cousin else None
+        parent = np.zeros((st["nseg"][d - 1], st["P"]), dtype=np.complex128) if what & 2 else None
+        _check(_lib.ifgf_debug_level_pass(self._h, int(d), v.ctypes.data, what,
+                                          field.ctypes.data if field is not None else None,
+                                          parent.ctypes.data if parent is not None else None),
+               "ifgf_debug_level_pass")
+        return field, parent
 
     def profile_enable(self, on: bool = True):
         _check(_lib.ifgf_profile_enable(self._h, 1 if on else 0), "ifgf_profile_enable")
