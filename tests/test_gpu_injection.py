@@ -136,8 +136,8 @@ def expected_parent_values(g, pts, d, poly, psegs):
     cell = psegs[:, 3]
     i_s, i_t, i_p = cell % nsP, (cell // nsP) % nCP, cell // (nsP * nCP)
     s = (i_s[:, None, None, None] + (1 + ts[None, None, None, :]) / 2) * dsP
-    th = (i_t[:, None, :, None] + (1 + ta[None, None, :, None]) / 2) * dthP
-    ph = (i_p[:, :, None, None] + (1 + ta[None, :, None, None]) / 2) * dthP
+    th = (i_t[:, None, None, None] + (1 + ta[None, None, :, None]) / 2) * dthP
+    ph = (i_p[:, None, None, None] + (1 + ta[None, :, None, None]) / 2) * dthP
     s, th, ph = np.broadcast_arrays(s, th, ph)                  # [seg, c, b, a]
     rQ = (math.sqrt(3) / 2 * g.H(dp)) / s
     off = np.stack([rQ * np.sin(th) * np.cos(ph), rQ * np.sin(th) * np.sin(ph), rQ * np.cos(th)], axis=-1)
