@@ -1067,6 +1067,11 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
     const int s1 = (c + 1 < LP.nchunk) ? LP.chunk_start[c + 1] : (int)LP.nseg;
     const int cnt = min(J, s1 - s0);
 
+    // per-octant task tables (phase 2): r -> (cell << 8 | node tile), r -> end of the cell's run
+    __shared__ unsigned short sTk[8][C::NR + C::UM + 1];
+    __shared__ unsigned char sGe[8][C::NR + C::UM + 1];
+    __shared__ int sS[8];
+
     // ---- phase 0
     __shared__ int sBox[J];
     __shared__ unsigned char sQd[J];  // quarter turns of segment j's cell from the representative
@@ -1195,6 +1200,27 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
             sUis[o * NW + pos] = 0xFF;
         }
         if (lane == 0) sUn[o] = U;
+        // task table of the octant: the node tiles of each child cell in cell order,
+        // r -> (cell, tile) and r -> end of that cell's run (lane u = cell u)
+        __syncwarp();
+        if (U <= UM) {
+            const unsigned char* ps = sPst + o * (UM + 1);
+            const int nt_u = lane < U ? ((ps[lane + 1] - 1) >> 3) - (ps[lane] >> 3) + 1 : 0;
+            int r0 = nt_u;
+#pragma unroll
+            for (int sh = 1; sh < 32; sh <<= 1) {
+                const int v = __shfl_up_sync(~0u, r0, sh);
+                if (lane >= sh) r0 += v;
+            }
+            const int rend = r0;  // inclusive prefix: end of this cell's run
+            r0 -= nt_u;
+            if (lane < U)
+                for (int q = 0; q < nt_u; ++q) {
+                    sTk[o][r0 + q] = (unsigned short)((lane << 8) | ((ps[lane] >> 3) + q));
+                    sGe[o][r0 + q] = (unsigned char)rend;
+                }
+            if (lane == 31) sS[o] = rend;
+        }
     }
     __syncthreads();
     mark(2);
@@ -1293,8 +1319,7 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
             // current group's node tiles run (register double buffer).
             const int nst = (no + 7) >> 3;
             const unsigned char* pst = sPst + o * (UM + 1);
-            int S = 0;
-            for (int u = 0; u < U; ++u) S += ((pst[u + 1] - 1) >> 3) - (pst[u] >> 3) + 1;
+            const int S = sS[o];
             const int T = nst * S;
             if (phase_clk && tid == 0) {  // shape counters: cells, node tiles, segments, octants
                 atomicAdd(phase_clk + 9, (unsigned long long)U);
@@ -1303,21 +1328,15 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
                 atomicAdd(phase_clk + 12, 1ull);
             }
             const int tau0 = (int)((int64_t)warp * T / NWARP), tau1 = (int)((int64_t)(warp + 1) * T / NWARP);
-            // decode task tau -> (st, ui, first tile of ui, tiles left in the group)
-            auto decode = [&](int tau, int& st, int& ui, int& tl0, int& off) {
+            // decode task tau -> (segment tile, child cell, its node tile, end of the
+            // (segment tile, cell) group) from the octant's task table
+            auto decode = [&](int tau, int& st, int& ui, int& tile, int& gend) {
                 st = tau / S;
-                int r = tau - st * S;
-                ui = 0;
-                while (true) {
-                    const int a0 = pst[ui] >> 3, n_t = ((pst[ui + 1] - 1) >> 3) - a0 + 1;
-                    if (r < n_t) {
-                        tl0 = a0;
-                        off = r;
-                        break;
-                    }
-                    r -= n_t;
-                    ++ui;
-                }
+                const int r = tau - st * S;
+                const int e = sTk[o][r];
+                ui = e >> 8;
+                tile = e & 0xFF;
+                gend = min(tau1, st * S + (int)sGe[o][r]);
             };
             auto load_b = [&](int st, int ui, double2* bb) {
                 const int q = st * 8 + gid;
@@ -1329,21 +1348,19 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
             };
             double2 bc[KS], bn[C::PREFETCH ? KS : 1];
             int tau = tau0;
-            int st = 0, ui = 0, tl0 = 0, off = 0;
+            int st = 0, ui = 0, tl = 0, gend = 0;
             if (tau < tau1) {
-                decode(tau, st, ui, tl0, off);
+                decode(tau, st, ui, tl, gend);
                 load_b(st, ui, bc);
             }
             while (tau < tau1) {
-                const int ntl = ((pst[ui + 1] - 1) >> 3) - tl0 + 1;
-                const int gend = min(tau1, tau + (ntl - off));  // end of this (st, ui) group
-                int st2 = 0, ui2 = 0, tl02 = 0, off2 = 0;
+                int st2 = 0, ui2 = 0, tl2 = 0, gend2 = 0;
                 if (gend < tau1) {
-                    decode(gend, st2, ui2, tl02, off2);
+                    decode(gend, st2, ui2, tl2, gend2);
                     if constexpr (C::PREFETCH) load_b(st2, ui2, bn);
                 }
                 const int p0 = pst[ui], p1 = pst[ui + 1];
-                for (int tile = tl0 + off; tile < tl0 + off + (gend - tau); ++tile) {
+                for (int tile = tl; tile < tl + (gend - tau); ++tile) {
                     const int pos = tile * 8 + gid;
                     const double* wr = sW + pos * KP + tig;
                     double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
@@ -1384,8 +1401,8 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
                 if (tau < tau1) {
                     st = st2;
                     ui = ui2;
-                    tl0 = tl02;
-                    off = off2;
+                    tl = tl2;
+                    gend = gend2;
                     if constexpr (C::PREFETCH) {
 #pragma unroll
                         for (int ks = 0; ks < KS; ++ks) bc[ks] = bn[ks];

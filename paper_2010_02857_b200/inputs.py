@@ -149,5 +149,15 @@ EXTRA_CONFIGS = {
                          geometry="prolate", notes="f3: 512 lambda along z, leaves lambda/4"),
     "rough4": Config("rough4", 25_165_824, 128 * math.pi, 10, 3, 5, geometry="rough",
                      notes="f3: rough sphere r = 1 + 0.05 sin(40 theta) sin(40 phi)"),
+    # f3: Table timings2: kappa sweep at fixed N = 393,216 on the sphere,
+    # leaves lambda/4 (D = 7, 8, 9 for kappa a = 16, 32, 64 pi)
+    "t4_16pi": Config("t4_16pi", 393_216, 16 * math.pi, 7, 3, 5, notes="f3 T4: kappa a = 16 pi, N fixed"),
+    "t4_32pi": Config("t4_32pi", 393_216, 32 * math.pi, 8, 3, 5, notes="f3 T4: kappa a = 32 pi, N fixed"),
+    "t4_64pi": Config("t4_64pi", 393_216, 64 * math.pi, 9, 3, 5, notes="f3 T4: kappa a = 64 pi, N fixed"),
+    # f3: Table timings3: N sweep at fixed kappa a = 16 pi (D = 7, leaves lambda/4)
+    "t5_24k": Config("t5_24k", 24_576, 16 * math.pi, 7, 3, 5, notes="f3 T5: N = 24,576 at 16 pi"),
+    "t5_98k": Config("t5_98k", 98_304, 16 * math.pi, 7, 3, 5, notes="f3 T5: N = 98,304 at 16 pi"),
+    "t5_393k": Config("t5_393k", 393_216, 16 * math.pi, 7, 3, 5, notes="f3 T5: N = 393,216 at 16 pi"),
+    "t5_1573k": Config("t5_1573k", 1_572_864, 16 * math.pi, 7, 3, 5, notes="f3 T5: N = 1,572,864 at 16 pi"),
 }
 

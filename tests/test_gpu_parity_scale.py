@@ -159,3 +159,26 @@ def test_k7_multi_tile_and_chunk_order(ifgf, env, monkeypatch):
     ref = oracle.OraclePlan(pts, k, D, 3, 5).apply(a)
     assert oracle.rel_l2(got, ref) <= PARITY
     assert element_max(got, ref) <= ELEMENT
+
+
+@pytest.mark.parametrize("n,kpi,D", [(24_576, 16, 7), (98_304, 32, 8)])
+def test_f3_sweeps_parity(ifgf, n, kpi, D):
+    """SURVEY.md §8(f) f3 sweeps at oracle-checkable sizes, leaves lambda/4
+    (P:2056-2059): the N sweep at kappa a = 16 pi (Table timings3; its
+    first row, N = 24,576, D = 7) and the kappa sweep (Table timings2)
+    at kappa a = 32 pi on N = 98,304 (D = 8).  All N targets, per-level segment
+    counts, and the error against the direct sum within 1.1x the oracle's."""
+    k = kpi * math.pi
+    pts, a = inputs.fibonacci_sphere(n), inputs.densities(n)
+    oplan = oracle.OraclePlan(pts, k, D, 3, 5)
+    ref = oplan.apply(a)
+    plan = ifgf.Plan(dev(pts), k, D, 3, 5)
+    got = plan.apply(dev(a)).cpu().numpy()
+    st = plan.stats()
+    assert oracle.rel_l2(got, ref) <= PARITY
+    assert element_max(got, ref) <= ELEMENT
+    for d in range(3, D + 1):
+        assert st["nseg"][d] == oplan.level_info(d)["nseg"]
+    tg = inputs.error_targets(n, 1000)
+    exact = ifgf.direct(dev(pts), k, dev(a), dev(tg)).cpu().numpy()
+    assert oracle.rel_l2(got[tg], exact) <= 1.1 * oracle.rel_l2(ref[tg], exact)
