@@ -382,3 +382,40 @@ def test_upward_kernel_variants(ifgf, mode, umax, monkeypatch):
     _, got, _ = run_gpu(ifgf, pts, a, k, 5)
     ref = oracle.OraclePlan(pts, k, 5, 3, 5).apply(a)
     assert oracle.rel_l2(got, ref) <= PARITY
+
+
+def lattice_shell(spacing=1.0 / 32, radius=0.8, width=1.0 / 40):
+    """Points on the lattice -1 + m * spacing inside a thin spherical shell: with
+    root box centre 0 and side 2 (x0 = -1), box faces and centres of every level
+    lie on the same lattice, so relative vectors x - c_B hit exact ties of the
+    interval rules (R7): poles (v_x = v_y = 0), v_z = 0 (theta = pi/2,
+    a boundary of every even n_C), the phi = j pi/2 half-planes and the phi = pi/4
+    diagonals (equal cos/sin table entries), and points on box faces."""
+    m = np.arange(-int(1 / spacing), int(1 / spacing) + 1)
+    g = -1.0 + (m + int(1 / spacing)) * spacing
+    X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+    P = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1)
+    r = np.linalg.norm(P, axis=1)
+    return np.ascontiguousarray(P[np.abs(r - radius) < width])
+
+
+@pytest.mark.parametrize("k,D", [(12.0, 5), (20.0, 6)])
+def test_lattice_boundary_ties(ifgf, k, D):
+    """Exact boundary ties of the classification against the oracle: identical
+    relevant boxes and segment sets per level (plan-diff) and field parity."""
+    pts = lattice_shell()
+    root = ([0.0, 0.0, 0.0], 2.0)
+    a = inputs.densities(len(pts), seed=41)
+    plan, got, st = run_gpu(ifgf, pts, a, k, D, root=root)
+    oplan = oracle.OraclePlan(pts, k, D, 3, 5, root=root)
+    ref = oplan.apply(a)
+    for d in range(1, D + 1):
+        assert st["nbox"][d] == oplan.level_info(d)["nbox"]
+        np.testing.assert_array_equal(segs_sorted(plan.level_segments(d)), segs_sorted(oplan.level_segments(d)))
+    assert oracle.rel_l2(got, ref) <= PARITY
+    # ties really occur: cousin points on the poles / on the phi half-planes of some box
+    x0 = -1.0
+    H = 2.0 / 2 ** (D - 1)
+    q = np.floor((pts - x0) / H)
+    c = x0 + (q + 0.5) * H
+    assert np.any(pts[:, 0] == c[:, 0]) and np.any(pts[:, 2] == c[:, 2])
