@@ -12,7 +12,7 @@ inputs resident in HBM.  Prints ONE JSON line on rank 0.
 
 --impl reference times the oracle (oracle/, C++ with its deterministic OpenMP
 mode on all host cores) on a bounded sample of the same workload: the partial
-apply of a 1/256 Morton slice of the leaves (sources) over all N targets,
+apply of a 1/128 Morton slice of the leaves (sources) over all N targets,
 extrapolated by the slice's share of the sources (rank 0 only).
 """
 from __future__ import annotations
@@ -39,16 +39,21 @@ METRIC = "IFGF matvec points/s (fp64 complex) at 1/2/4/8 B200; rel. error vs dir
 UNIT = "points/s"
 
 # Bounded CPU sample of the oracle (cpu_baseline and --impl reference): the oracle
-# plan of the SAME workload owning a contiguous Morton slice of 1/256 of the leaf
-# boxes (source partition); one step = its partial apply over all
-# N targets; points/s = (owned sources / N) * N / t, i.e. the full apply's rate if
-# its time scaled with the sources (coarse ancestors of the slice are shared, so
-# the slice costs a little more than 1/256: a conservative estimate).
-CPU_SLICE = (0.45, 1.0 / 256)
+# plan of the SAME workload owning a contiguous Morton slice of the leaf boxes
+# (source partition); one step = its partial apply over all N
+# targets; points/s = (owned sources / N) * N / t, i.e. the full apply's rate if its
+# time scaled with the sources.  The slice's coarse ancestors carry whole-box cone
+# data, so a slice costs more than its share (a conservative estimate): on cfg4 with
+# 16 host cores the full apply measured 495 s (50.8 k points/s,
+# profiles/r02/parity_full_cfg4.json).  cpu_baseline: 1/32 of the leaves (one step,
+# ~20 s); --impl reference: 1/128 per step, so K + W steps end within minutes.
+CPU_SLICE_START = 0.45
+CPU_SLICE_BASELINE = 1.0 / 32
+CPU_SLICE_REFERENCE = 1.0 / 128
 
 
 class OracleSample:
-    def __init__(self, c):
+    def __init__(self, c, frac_leaves: float):
         import oracle
         oracle.set_threads(0)
         self.cores = oracle.get_threads()
@@ -65,8 +70,8 @@ class OracleSample:
             for ax, sh in ((0, 2), (1, 1), (2, 0)):
                 key |= ((q[:, ax] >> np.uint64(bit)) & np.uint64(1)) << np.uint64(3 * bit + sh)
         leaves = np.unique(key)
-        i0 = int(CPU_SLICE[0] * len(leaves))
-        i1 = i0 + max(1, int(CPU_SLICE[1] * len(leaves)))
+        i0 = int(CPU_SLICE_START * len(leaves))
+        i1 = i0 + max(1, int(frac_leaves * len(leaves)))
         lo, hi = int(leaves[i0]), int(leaves[min(i1, len(leaves) - 1)])
         self.frac = float(np.mean((key >= np.uint64(lo)) & (key < np.uint64(hi))))
         self.plan = oracle.OraclePlan(pts, c.k, c.levels, c.Ps, c.Pang, owned_morton=(lo, hi))
@@ -178,7 +183,7 @@ def run_reference(args, rank: int):
     if rank != 0:
         return
     c = ALL_CONFIGS[args.config]
-    smp = OracleSample(c)
+    smp = OracleSample(c, CPU_SLICE_REFERENCE)
     ts = [smp.step() for _ in range(args.warmup + args.steps)]
     timed = ts[args.warmup:] if len(ts) > args.warmup else ts
     t = sum(timed) / len(timed)
@@ -311,7 +316,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            smp = OracleSample(c)
+            smp = OracleSample(c, CPU_SLICE_BASELINE)
             ts = [smp.step() for _ in range(args.cpu_repeats)]
             cpu = {"value": smp.value(statistics.median(ts)), "unit": UNIT, "cores": smp.cores, "kind": "oracle",
                    "sample": smp.desc + f"; median of {len(ts)} steps ({sum(ts):.1f} s wall, after "
@@ -353,7 +358,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4", choices=sorted(inputs.CONFIGS) + sorted(inputs.EXTRA_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-repeats", type=int, default=2)
+    ap.add_argument("--cpu-repeats", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -108,6 +108,15 @@ __global__ void k_unpermute(const double2* __restrict__ in, const int* __restric
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) out[perm[i]] = in[i];
 }
+// out[perm[i]] = far[i] + near[i]: the cousin sum (levels D..3) plus the near field
+__global__ void k_unpermute_sum(const double2* __restrict__ far, const double2* __restrict__ near,
+                                const int* __restrict__ perm, int64_t n, double2* out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double2 a = far[i], b = near[i];
+        out[perm[i]] = make_double2(a.x + b.x, a.y + b.y);
+    }
+}
 
 // K3: out[l] = sum over owned neighbour boxes B of the leaf T containing l,
 // sum_{m in B, m != l} a_m e^{ik r}/(4 pi r)  (raw kernel, reading R11).
@@ -1960,42 +1969,63 @@ void upward_level(ifgf_plan_s* p, int d, cudaStream_t st) {
     if (!fused) fit_level(p, d - 1, st);
 }
 
-void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t st) {
-    const int D = p->D, P = p->P, Ps = p->Ps, Pa = p->Pa;
+// One apply (Algorithm 1).  The near field (K3) accumulates into its
+// own buffer; the cousin interpolation (K6, levels D..3 in order) into out_sorted;
+// the un-permute adds the two (the same order whether or not the kernels overlap).
+// conc (graph capture): three streams -- K3 || (K4, K5, K7 chain) || K6 chain,
+// with K6(d) after level d's values and K7(d -> d-1) after K6(d+1) (it overwrites
+// level d+1's buffer); otherwise everything runs in order on st.
+void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t st, bool conc) {
+    const int D = p->D, Ps = p->Ps, Pa = p->Pa;
     const int64_t n = p->n;
     const unsigned mask = p->stage_mask;
+    if (conc && !p->side[0]) {
+        for (int i = 0; i < 2; ++i) IFGF_CUDA(cudaStreamCreateWithFlags(&p->side[i], cudaStreamNonBlocking));
+        p->ev.resize(2 * (D + 2) + 2);
+        for (auto& e : p->ev) IFGF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t sN = conc ? p->side[0] : st, sU = conc ? p->side[1] : st;
+    auto ev_lev = [&](int d) { return p->ev[d]; };
+    auto ev_cou = [&](int d) { return p->ev[(D + 2) + d]; };
+    cudaEvent_t ev_fork = conc ? p->ev[2 * (D + 2)] : nullptr, ev_near = conc ? p->ev[2 * (D + 2) + 1] : nullptr;
     {
         Prof pr(p, st, 0);
         k_permute<<<nblk(n, 256), 256, 0, st>>>(dens, p->perm, n, p->a_sorted);
         pr.done();
     }
-    LevelHost& LD = p->lev[D];
-    if (mask & IFGF_STAGE_NEAR) {
-        Prof pr(p, st, 1);
-        if (p->nranks > 1)  // targets without an owned neighbour get no near-field work item
-            IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));
-        k_near<<<nblk(LD.p.nwitems_near * 32), TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k,
-                                                               p->out_sorted);
-        pr.done();
-    } else {
-        IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));
+    if (conc) {
+        IFGF_CUDA(cudaEventRecord(ev_fork, st));
+        IFGF_CUDA(cudaStreamWaitEvent(sN, ev_fork, 0));
+        IFGF_CUDA(cudaStreamWaitEvent(sU, ev_fork, 0));
     }
+    LevelHost& LD = p->lev[D];
+    const bool near = mask & IFGF_STAGE_NEAR;
+    if (near) {
+        Prof pr(p, sN, 1);
+        if (p->nranks > 1)  // targets without an owned neighbour get no near-field work item
+            IFGF_CUDA(cudaMemsetAsync(p->near_sorted, 0, sizeof(double2) * n, sN));
+        k_near<<<nblk(LD.p.nwitems_near * 32), TPB, 0, sN>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k,
+                                                               p->near_sorted);
+        pr.done();
+        if (conc) IFGF_CUDA(cudaEventRecord(ev_near, sN));
+    }
+    IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));
     bool have = false;        // level d holds coefficients
     bool leaf_fused = false;  // K4 fused the leaf-level fit
     if (D >= 3 && (mask & (IFGF_STAGE_COUSIN | IFGF_STAGE_UPWARD)) && LD.p.b1 > LD.p.b0) {
         if (LD.p.nseg > 0) {
-            Prof pr(p, st, 2);
+            Prof pr(p, sU, 2);
             const unsigned nb = (unsigned)(LD.p.b1 - LD.p.b0);
             if (LD.p.ncell <= 8 && Ps == 3 && Pa == 5) {
-                k_s2c<3, 5><<<nb, TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
+                k_s2c<3, 5><<<nb, TPB, 0, sU>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
                                                 p->cheb_Ms, p->cheb_Ma);
                 leaf_fused = true;
             } else if (LD.p.ncell <= 8 && Ps == 5 && Pa == 5) {
-                k_s2c<5, 5><<<nb, TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
+                k_s2c<5, 5><<<nb, TPB, 0, sU>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
                                                 p->cheb_Ms, p->cheb_Ma);
                 leaf_fused = true;
             } else {
-                k_s2c<0, 0><<<nb, TPB, 0, st>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
+                k_s2c<0, 0><<<nb, TPB, 0, sU>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
                                                 p->cheb_Ms, p->cheb_Ma);
             }
             pr.done();
@@ -2019,19 +2049,35 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
                 (double)h[10] / std::max(1.0, (double)h[12]), (double)h[11] / std::max(1.0, (double)h[12]),
                 (double)h[12] / std::max(1.0, (double)h[13]));
     };
-    if (have && !leaf_fused) fit_level(p, D, st);
+    if (have && !leaf_fused) fit_level(p, D, sU);
+    if (conc && have) IFGF_CUDA(cudaEventRecord(ev_lev(D), sU));
     for (int d = D; d >= 3 && have; --d) {
-        if (mask & IFGF_STAGE_COUSIN) cousin_level(p, d, st);
+        if (mask & IFGF_STAGE_COUSIN) {
+            if (conc) IFGF_CUDA(cudaStreamWaitEvent(st, ev_lev(d), 0));
+            cousin_level(p, d, st);
+        }
+        if (conc) IFGF_CUDA(cudaEventRecord(ev_cou(d), st));
         if (d > 3 && (mask & IFGF_STAGE_UPWARD)) {
-            upward_level(p, d, st);
+            // K7 (d -> d-1) overwrites level d+1's buffer: after K6(d+1)
+            if (conc && d < D) IFGF_CUDA(cudaStreamWaitEvent(sU, ev_cou(d + 1), 0));
+            upward_level(p, d, sU);
+            if (conc) IFGF_CUDA(cudaEventRecord(ev_lev(d - 1), sU));
             phase_dump(d - 1);
         } else {
             have = false;
         }
     }
+    if (conc) {  // join: the near field and the upward chain
+        if (near) IFGF_CUDA(cudaStreamWaitEvent(st, ev_near, 0));
+        IFGF_CUDA(cudaEventRecord(ev_fork, sU));
+        IFGF_CUDA(cudaStreamWaitEvent(st, ev_fork, 0));
+    }
     {
         Prof pr(p, st, 6);
-        k_unpermute<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->perm, n, out);
+        if (near)
+            k_unpermute_sum<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->near_sorted, p->perm, n, out);
+        else
+            k_unpermute<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->perm, n, out);
         pr.done();
     }
 }

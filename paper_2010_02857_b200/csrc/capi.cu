@@ -56,6 +56,9 @@ void free_plan(ifgf_plan_s* p) {
     if (!p) return;
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+    for (auto& sd : p->side)
+        if (sd) cudaStreamDestroy(sd);
+    for (auto& e : p->ev) cudaEventDestroy(e);
     for (void* a : p->allocs) cudaFree(a);
     for (auto& e : p->ev_pool) cudaEventDestroy(e);
     for (auto& e : p->pending) {
@@ -83,7 +86,7 @@ void apply_dispatch(ifgf_plan_s* p, const double2* dens, double2* out, cudaStrea
             cudaGraph_t g = nullptr;
             bool ok = true;
             try {
-                ifgf::run_apply(p, dens, out, p->cap_stream);
+                ifgf::run_apply(p, dens, out, p->cap_stream, !p->no_concurrency);
             } catch (const ifgf::Error&) {
                 ok = false;
             }
@@ -106,7 +109,7 @@ void apply_dispatch(ifgf_plan_s* p, const double2* dens, double2* out, cudaStrea
             done = true;
         }
     }
-    if (!done) ifgf::run_apply(p, dens, out, st);
+    if (!done) ifgf::run_apply(p, dens, out, st, false);
     if (p->nccl_comm)  // the one exchange step of the source partition
         IFGF_NCCL(ncclAllReduce(out, out, (size_t)2 * p->n, ncclDouble, ncclSum, (ncclComm_t)p->nccl_comm, st));
 }
@@ -299,6 +302,7 @@ ifgf_status ifgf_plan(const double* points, int64_t n, double k, int levels, int
     p->rank = o.nranks > 1 ? o.rank : 0;
     p->nranks = o.nranks > 1 ? o.nranks : 1;
     p->use_graph = !o.no_graph && !std::getenv("IFGF_NO_GRAPH");
+    p->no_concurrency = std::getenv("IFGF_NO_CONCURRENCY") != nullptr;
     if (o.nccl_comm) {
         int cnt = 0, rk = 0;
         if (ncclCommCount((ncclComm_t)o.nccl_comm, &cnt) != ncclSuccess ||

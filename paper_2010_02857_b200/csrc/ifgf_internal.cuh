@@ -141,7 +141,8 @@ struct ifgf_plan_s {
     double* cheb_Ma = nullptr;  // Pa x Pa
     // apply scratch
     double2* a_sorted = nullptr;
-    double2* out_sorted = nullptr;
+    double2* out_sorted = nullptr;   // cousin (K6) sum, Morton order
+    double2* near_sorted = nullptr;  // near field (K3), Morton order
     double2* vals[2] = {nullptr, nullptr};  // ping-pong by level parity (+1 zeroed tail segment)
     double2* zseg = nullptr;                // P + 4 zeros: the TC K7's absent-column operand
     int64_t vals_cap[2] = {0, 0};
@@ -174,11 +175,14 @@ struct ifgf_plan_s {
     // CUDA graph of one apply (captured on cap_stream for one (densities, out) pair,
     // replayed on the caller's stream)
     bool use_graph = true;
+    bool no_concurrency = false;  // env IFGF_NO_CONCURRENCY: captured apply on one stream (A/B)
     bool graph_failed = false;
     cudaStream_t cap_stream = nullptr;
     cudaGraphExec_t gexec = nullptr;
     const void* g_dens = nullptr;
     void* g_out = nullptr;
+    cudaStream_t side[2] = {nullptr, nullptr};  // captured apply: K3 stream, K4/K5/K7 stream
+    std::vector<cudaEvent_t> ev;                // their fork / join / per-level events
 };
 
 namespace ifgf {
@@ -196,7 +200,7 @@ T* dev_alloc(ifgf_plan_s* p, int64_t count) {
 void dev_free(ifgf_plan_s* p, void* ptr);
 
 void build_plan(ifgf_plan_s* p, const double* points_dev, const ifgf_opts& o);
-void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t st);
+void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t st, bool conc);
 void debug_level_pass(ifgf_plan_s* p, int d, const double2* values_h, unsigned what, double2* field_h,
                       double2* parent_h);
 

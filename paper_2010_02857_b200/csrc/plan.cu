@@ -1388,6 +1388,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
     // 9. apply scratch: permuted densities, sorted field, two segment-value levels
     p->a_sorted = dev_alloc<double2>(p, n);
     p->out_sorted = dev_alloc<double2>(p, n);
+    p->near_sorted = dev_alloc<double2>(p, n);
     for (int par = 0; par < 2; ++par) {
         int64_t mx = 0;
         for (int d = 3; d <= D; ++d)
