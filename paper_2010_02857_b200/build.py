@@ -29,9 +29,13 @@ NCCL_INC = ["-I", os.path.join(NCCL_DIR, "include")] if NCCL_DIR else []
 NCCL_LINK = (["-L", os.path.join(NCCL_DIR, "lib"), "-Xlinker", "-rpath=" + os.path.join(NCCL_DIR, "lib")]
              if NCCL_DIR else []) + ["-l:libnccl.so.2"]
 
+# IFGF_CHECKS=1: debug build with device-side bounds checks (IFGF_DCHECK).
+CHECKS = os.environ.get("IFGF_CHECKS", "0") not in ("", "0")
+
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
+    *(["-DIFGF_CHECKS"] if CHECKS else []),
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
@@ -47,6 +51,9 @@ def _newest_input_mtime() -> float:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    stamp = LIB + ".checks"
+    if CHECKS != os.path.exists(stamp):
+        force = True  # switching between the release and the bounds-checked build
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_input_mtime():
         return LIB
     objs = []
@@ -67,6 +74,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
     os.replace(tmp, LIB)
+    if CHECKS:
+        open(stamp, "w").close()
+    elif os.path.exists(stamp):
+        os.remove(stamp)
     with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:

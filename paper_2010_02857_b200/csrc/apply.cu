@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
             v.up = c.up;
         }
         v.bi = stage_distinct<P>(v.slot, lane, min(SMAX, smax), vals, &sbuf[w][buf][0][0], SP, &sbar[w][buf]);
+        IFGF_DCHECK(v.bi < SMAX && v.slot < L.nseg);
     };
     double ar = 0.0, ai = 0.0;
     const int niter = (e1 - e0 + step - 1) / step;
@@ -564,6 +565,7 @@ __global__ void __launch_bounds__(PE_WARPS * 32, 5) k_upward_pe(LevelParams L, L
             v.up = c.up;
         }
         v.bi = stage_distinct<P>(v.slot, lane, min(SMAX, smax), vals_d, &sbuf[w][buf][0][0], SP, &sbar[w][buf]);
+        IFGF_DCHECK(v.bi < SMAX && v.slot < L.nseg);
     };
     // octants with a child for some lane of the warp (the others are skipped)
     unsigned mymask = 0u;
@@ -1349,7 +1351,9 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
             };
             auto load_b = [&](int st, int ui, double2* bb) {
                 const int q = st * 8 + gid;
+                IFGF_DCHECK(ui >= 0 && ui < UM && st >= 0 && st * 8 < J);
                 const int sl = q < no ? sSlot[(o * UM + ui) * J + q] : -1;
+                IFGF_DCHECK(sl < L.nseg);
                 const double2* cp = sl >= 0 ? vals_d + (int64_t)sl * P : zseg;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks)  // k = 4 ks + tig >= P (last step): zero, not the next segment
@@ -1371,6 +1375,7 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
                 const int p0 = pst[ui], p1 = pst[ui + 1];
                 for (int tile = tl; tile < tl + (gend - tau); ++tile) {
                     const int pos = tile * 8 + gid;
+                    IFGF_DCHECK(tile >= 0 && tile < C::NR);
                     const double* wr = sW + pos * KP + tig;
                     double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
                     double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
@@ -1397,6 +1402,7 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
                             const int qq = st * 8 + 2 * tig + h;
                             if (qq < no) {
                                 const int j = sJl[o * J + qq];
+                                IFGF_DCHECK(j < J && n < P);
                                 const double fr = h ? dr1 : dr0, fi = h ? di1 : di0;
                                 double2 acc = sV[j * P + n];
                                 acc.x = fma(rr, fr, fma(-ri, fi, acc.x));

@@ -26,6 +26,24 @@ struct Error {
     std::string msg;
 };
 void set_error(const std::string& msg);
+// Device-side bounds checks of the debug build (IFGF_CHECKS=1 at build time; the
+// stand-in for compute-sanitizer, which this GPU pool does not allow): a failed
+// check prints its location and traps (the apply then returns IFGF_ECUDA).
+#ifdef IFGF_CHECKS
+#define IFGF_DCHECK(cond)                                                                     \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("IFGF_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,  \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                              \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define IFGF_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 #define IFGF_CUDA(call)                                                                              \
     do {                                                                                             \
         cudaError_t e_ = (call);                                                                     \
@@ -302,11 +320,14 @@ __device__ __forceinline__ int64_t cell_of(const LevelParams& L, const Cls& c) {
 // Slot of (box b, cell) among the level's relevant segments (O(1) rank lookup),
 // or -1 if the segment is not relevant.
 __device__ __forceinline__ int64_t seg_slot(const LevelParams& L, int64_t b, int64_t cell) {
+    IFGF_DCHECK(b >= L.b0 && b < L.b1 && cell >= 0 && cell < L.ncell);
     int64_t w = (b - L.b0) * L.W + (cell >> 6);
     unsigned long long word = __ldg(L.bitmap + w);
     unsigned long long bit = 1ull << (cell & 63);
     if (!(word & bit)) return -1;
-    return (int64_t)__ldg(L.rank + w) + __popcll(word & (bit - 1));
+    const int64_t slot = (int64_t)__ldg(L.rank + w) + __popcll(word & (bit - 1));
+    IFGF_DCHECK(slot >= 0 && slot < L.nseg);
+    return slot;
 }
 
 __device__ __forceinline__ double box_centre(const LevelParams& L, int k, int axis) {
