@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
                                                    const double2* __restrict__ vals, double k, double2* out,
                                                    int* bad, int smax) {
     constexpr int P = PS * PA * PA;
-    constexpr int SMAX = P <= 80 ? 4 : 2;  // static shared memory <= 48 KB per block
+    constexpr int SMAX = P <= 80 ? 4 : (P <= 128 ? 2 : 1);  // static shared memory <= 48 KB per block
     constexpr int SP = P + 2;  // slot stride (double2): 4 slots -> disjoint banks for 16-byte reads
     __shared__ __align__(16) double2 sbuf[TPB / 32][2][SMAX][SP];
     __shared__ __align__(8) unsigned long long sbar[TPB / 32][2];
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(PE_WARPS * 32, 5) k_upward_pe(LevelParams L, L
                                                       const double2* __restrict__ vals_d, double k, double2* vals_p,
                                                       int* bad, int smax) {
     constexpr int P = PS * PA * PA;
-    constexpr int SMAX = P <= 80 ? PE_SMAX : 2;
+    constexpr int SMAX = P <= 80 ? PE_SMAX : (P <= 128 ? 2 : 1);
     constexpr int SP = P + 2;
     __shared__ __align__(16) double2 sbuf[PE_WARPS][2][SMAX][SP];
     __shared__ __align__(8) unsigned long long sbar[PE_WARPS][2];
@@ -1025,8 +1025,7 @@ struct TcCfg {
     static constexpr size_t oMisc = a16(oUcell + (size_t)8 * UM * 4);     // int U[8], nO[8]
     static constexpr size_t oPst = a16(oMisc + 16 * 4);                   // u8 [8][UM + 1] run starts
     static constexpr size_t oOrd = a16(oPst + (size_t)8 * (UM + 1));      // u8 [8][NW]
-    static constexpr size_t oUis = a16(oOrd + (size_t)8 * NW);            // u8 [8][NW]
-    static constexpr size_t oJl = a16(oUis + (size_t)8 * NW);             // u8 [8][J]
+    static constexpr size_t oJl = a16(oOrd + (size_t)8 * NW);             // u8 [8][J]
     static constexpr size_t oFit = a16(oJl + (size_t)8 * J);              // double Ms, Ma
     static constexpr size_t smem = a16(oFit + (size_t)(PS * PS + PA * PA) * 8);
     static_assert(NWARP >= 8, "phase 0/2 map one warp per octant");
@@ -1066,7 +1065,6 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
     int* sNo = sUn + 8;
     unsigned char* sPst = smraw + C::oPst;
     unsigned char* sOrd = smraw + C::oOrd;
-    unsigned char* sUis = smraw + C::oUis;
     unsigned char* sJl = smraw + C::oJl;
     double* sMs = reinterpret_cast<double*>(smraw + C::oFit);
     double* sMa = sMs + PS * PS;
@@ -1197,7 +1195,6 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
                 if (hit) {
                     const int pos = base + __popc(b & lt);
                     sOrd[o * NW + pos] = (unsigned char)(lane + 32 * r);
-                    sUis[o * NW + pos] = (unsigned char)min(U, 254);
                     done[r] = true;
                 }
                 base += __popc(b);
@@ -1208,7 +1205,6 @@ __global__ void __launch_bounds__(TcCfg<PS, PA>::NT, 1) k_upward_tc(LevelParams 
         if (lane == 0 && U <= UM) sPst[o * (UM + 1) + U] = (unsigned char)base;
         for (int pos = base + lane; pos < NW; pos += 32) {
             sOrd[o * NW + pos] = (unsigned char)pos;
-            sUis[o * NW + pos] = 0xFF;
         }
         if (lane == 0) sUn[o] = U;
         // task table of the octant: the node tiles of each child cell in cell order,
@@ -1490,8 +1486,7 @@ struct Tc2Cfg {
     static constexpr size_t oMisc = a16(oUcell + (size_t)8 * UM * 4);     // int U[8], nO[8]
     static constexpr size_t oPst = a16(oMisc + 16 * 4);                   // u8 [8][UM + 1]
     static constexpr size_t oOrd = a16(oPst + (size_t)8 * (UM + 1));      // u8 [8][NW]
-    static constexpr size_t oUis = a16(oOrd + (size_t)8 * NW);            // u8 [8][NW]
-    static constexpr size_t oJl = a16(oUis + (size_t)8 * NW);             // u8 [8][J]
+    static constexpr size_t oJl = a16(oOrd + (size_t)8 * NW);             // u8 [8][J]
     static constexpr size_t oFit = a16(oJl + (size_t)8 * J);              // double Ms, Ma
     static constexpr size_t smem = a16(oFit + (size_t)(PS * PS + PA * PA) * 8);
     static_assert(2 * FG * P * 16 <= 8 * NW * 5 * 8, "fit temporaries alias the geometry");
@@ -1518,7 +1513,6 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
     int* sNo = sUn + 8;
     unsigned char* sPst = smraw + C::oPst;
     unsigned char* sOrd = smraw + C::oOrd;
-    unsigned char* sUis = smraw + C::oUis;
     unsigned char* sJl = smraw + C::oJl;
     double* sMs = reinterpret_cast<double*>(smraw + C::oFit);
     double* sMa = sMs + PS * PS;
@@ -1626,7 +1620,6 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
                 if (hit) {
                     const int pos = base + __popc(b & lt);
                     sOrd[o * NW + pos] = (unsigned char)(lane + 32 * r);
-                    sUis[o * NW + pos] = (unsigned char)min(U, 254);
                     done[r] = true;
                 }
                 base += __popc(b);
@@ -1637,7 +1630,6 @@ __global__ void __launch_bounds__(Tc2Cfg<PS, PA>::NT, 2) k_upward_tc2(LevelParam
         if (lane == 0 && U <= UM) sPst[o * (UM + 1) + U] = (unsigned char)base;
         for (int pos = base + lane; pos < NW; pos += 32) {
             sOrd[o * NW + pos] = (unsigned char)pos;
-            sUis[o * NW + pos] = 0xFF;
         }
         if (lane == 0) sUn[o] = U;
     }
@@ -1882,10 +1874,14 @@ struct Kern {
     }
 };
 
-template <class F3, class F5, class FG>
-void dispatch(int Ps, int Pa, F3 f35, F5 f55, FG fg) {
+// Orders with compiled specialisations: (3, 5) (the BASELINE configs), (5, 5) (cfg3)
+// and (5, 7) (the accuracy knob: ~20x lower error than (3, 5)); any
+// other order runs the runtime-order kernels.
+template <class F3, class F5, class F7, class FG>
+void dispatch(int Ps, int Pa, F3 f35, F5 f55, F7 f57, FG fg) {
     if (Ps == 3 && Pa == 5) f35();
     else if (Ps == 5 && Pa == 5) f55();
+    else if (Ps == 5 && Pa == 7) f57();
     else fg();
 }
 
@@ -1934,6 +1930,7 @@ void fit_level(ifgf_plan_s* p, int d, cudaStream_t st) {
     dispatch(
         Ps, Pa, [&] { k_fit_lines<3, 5><<<nb8, 64, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
         [&] { k_fit_lines<5, 5><<<nb8, 64, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
+        [&] { k_fit_lines<5, 7><<<nb8, 64, 0, st>>>(L.nseg, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]); },
         [&] {
             k_fit<<<(int)((L.nseg + fit_warps - 1) / fit_warps), 32 * fit_warps, fit_smem, st>>>(
                 L.nseg, Ps, Pa, p->cheb_Ms, p->cheb_Ma, p->vals[d & 1]);
@@ -1951,6 +1948,7 @@ void cousin_level(ifgf_plan_s* p, int d, cudaStream_t st) {
     dispatch(
         p->Ps, p->Pa, [&] { Kern<3, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
         [&] { Kern<5, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
+        [&] { Kern<5, 7>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
         [&] { Kern<0, 0>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); });
     pr.done();
 }
@@ -1969,6 +1967,7 @@ void upward_level(ifgf_plan_s* p, int d, cudaStream_t st) {
         dispatch(
             p->Ps, p->Pa, [&] { fused = Kern<3, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
             [&] { fused = Kern<5, 5>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
+            [&] { fused = Kern<5, 7>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); },
             [&] { fused = Kern<0, 0>::upward(g, st, L, LP, p, vd, vp, p->dev_bad); });
         pr.done();
     }
@@ -2028,6 +2027,10 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
                 leaf_fused = true;
             } else if (LD.p.ncell <= 8 && Ps == 5 && Pa == 5) {
                 k_s2c<5, 5><<<nb, TPB, 0, sU>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
+                                                p->cheb_Ms, p->cheb_Ma);
+                leaf_fused = true;
+            } else if (LD.p.ncell <= 8 && Ps == 5 && Pa == 7) {
+                k_s2c<5, 7><<<nb, TPB, 0, sU>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
                                                 p->cheb_Ms, p->cheb_Ma);
                 leaf_fused = true;
             } else {

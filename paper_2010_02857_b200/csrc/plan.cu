@@ -1220,7 +1220,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             if (P > 80 && kn == 1) kn = 0;  // TC kernel shared memory is sized for P <= 80 ((P_s, P_ang) = (3, 5))
             if (kn == 3 && !(Ps == 3 && Pa == 5)) kn = 1;  // TC v2 k-permutation is specific to (3, 5)
             // orders without a compiled specialisation run the generic per-evaluation kernel
-            if (!((Ps == 3 && Pa == 5) || (Ps == 5 && Pa == 5))) kn = 2;
+            if (!((Ps == 3 && Pa == 5) || (Ps == 5 && Pa == 5))) kn = 2;  // incl. (5, 7): specialised pe
             return kn;
         };
         int64_t nrun = 0;

@@ -139,7 +139,7 @@ def test_small_and_ragged(ifgf, n, D):
         assert oracle.rel_l2(got, ref) <= PARITY
 
 
-@pytest.mark.parametrize("Ps,Pa", [(5, 5), (4, 6), (1, 1), (2, 3), (7, 9)])
+@pytest.mark.parametrize("Ps,Pa", [(5, 5), (5, 7), (4, 6), (1, 1), (2, 3), (7, 9)])
 def test_orders_generic_and_specialised(ifgf, Ps, Pa):
     """(3,5) and (5,5) run specialised kernels; the rest the runtime-order path."""
     n = 6000
