@@ -104,17 +104,24 @@ __global__ void k_permute(const double2* __restrict__ in, const int* __restrict_
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) out[i] = in[perm[i]];
 }
-__global__ void k_unpermute(const double2* __restrict__ in, const int* __restrict__ perm, int64_t n, double2* out) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) out[perm[i]] = in[i];
-}
-// out[perm[i]] = far[i] + near[i]: the cousin sum (levels D..3) plus the near field
-__global__ void k_unpermute_sum(const double2* __restrict__ far, const double2* __restrict__ near,
-                                const int* __restrict__ perm, int64_t n, double2* out) {
+// out[perm[i]] = sum of the nfar cousin parts (levels D..3) + sum of the nnear
+// near-field parts, in that fixed order
+__global__ void k_unpermute_sum(const double2* __restrict__ far, int nfar, const double2* __restrict__ near,
+                                int nnear, const int* __restrict__ perm, int64_t n, double2* out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) {
-        const double2 a = far[i], b = near[i];
-        out[perm[i]] = make_double2(a.x + b.x, a.y + b.y);
+        double2 acc = far[i];
+        for (int q = 1; q < nfar; ++q) {
+            const double2 v = far[q * n + i];
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+        for (int q = 0; q < nnear; ++q) {
+            const double2 v = near[q * n + i];
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+        out[perm[i]] = acc;
     }
 }
 
@@ -123,14 +130,19 @@ __global__ void k_unpermute_sum(const double2* __restrict__ far, const double2* 
 // One warp per (leaf, 32 targets).  The neighbours' sources are staged per warp
 // in shared memory in chunks of 32 (one coalesced load per lane), then every
 // lane sweeps the chunk (broadcast reads); 1/r from one rsqrt, phase by fm::sincos.
+template <bool SPLIT>  // SPLIT (small problems only, nsplit_near > 1): nsplit warps per work item
 __global__ void __launch_bounds__(TPB, 8) k_near(LevelParams L, const double* __restrict__ px,
                                               const double* __restrict__ py, const double* __restrict__ pz,
                                               const double2* __restrict__ a, double k, double2* out) {
     __shared__ double sx[TPB / 32][32], sy[TPB / 32][32], sz[TPB / 32][32];
     __shared__ double2 sa[TPB / 32][32];
-    const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int nsplit = SPLIT ? L.nsplit_near : 1;
+    const int64_t item = SPLIT ? wid / nsplit : wid;
+    const int part = SPLIT ? (int)(wid - item * nsplit) : 0;  // this warp's share of the neighbour boxes
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (item >= L.nwitems_near) return;  // warp-uniform
+    if (SPLIT) out += (int64_t)part * (L.box_start[L.nbox]);  // field part (parts are n apart)
     const int2 it = L.witems_near[item];
     // items with <= 16 targets run split: lanes l and l + 16 take the same target
     // and alternate sources; the halves are summed at the end (fixed order)
@@ -147,7 +159,7 @@ __global__ void __launch_bounds__(TPB, 8) k_near(LevelParams L, const double* __
     }
     double ar = 0.0, ai = 0.0;
     const int e1 = L.nbr_off[T + 1];
-    for (int e = L.nbr_off[T]; e < e1; ++e) {
+    for (int e = L.nbr_off[T] + part; e < e1; e += nsplit) {
         const int B = L.nbr_idx[e];
         if (B < L.b0 || B >= L.b1) continue;
         const int m0 = L.box_start[B], m1 = L.box_start[B + 1];
@@ -221,11 +233,18 @@ __global__ void __launch_bounds__(TPB, 8) k_s2c(LevelParams L, const double* __r
     __shared__ double2 sV[FUSE ? 8 * PF : 1];
     __shared__ int sSeg[8];
     const int P = FUSE ? PF : Ps * Pa * Pa;
-    int64_t B = L.b0 + blockIdx.x;
+    // small problems (nsplit_s2c > 1): several blocks per leaf, each a contiguous share of its segments
+    const int64_t B = L.b0 + blockIdx.x / L.nsplit_s2c;
+    const int part = (int)(blockIdx.x % L.nsplit_s2c);
     __shared__ double sw[S2C_CHUNK][4];  // source - centre (x, y, z), |source - centre|^2
     __shared__ double2 sa[S2C_CHUNK];
     const int64_t row = (B - L.b0) * L.W;
-    const int64_t s0 = L.rank[row], s1 = L.rank[row + L.W];
+    int64_t s0 = L.rank[row], s1 = L.rank[row + L.W];
+    if (L.nsplit_s2c > 1) {
+        const int64_t q = (s1 - s0 + L.nsplit_s2c - 1) / L.nsplit_s2c;
+        s0 = min(s1, s0 + part * q);
+        s1 = min(s1, s0 + q);
+    }
     const int64_t nitem = (s1 - s0) * P;
     if (nitem == 0) return;
     double cx, cy, cz;
@@ -359,15 +378,18 @@ __global__ void __launch_bounds__(TPB) k_cousin(LevelParams L, const double* __r
                                                 const double2* __restrict__ vals, double k, int Ps, int Pa,
                                                 double2* out, int* bad) {
     const int P = Ps * Pa * Pa;
-    int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t item = wid / L.nsplit_cou;
+    const int part = (int)(wid - item * L.nsplit_cou);  // this warp's share of the cousin boxes
     int lane = threadIdx.x & 31;
     if (item >= L.nwitems) return;
+    out += (int64_t)part * (L.box_start[L.nbox]);
     int2 it = L.witems[item];
     int T = it.x, l = it.y + lane;
     if (l >= L.box_start[T + 1]) return;
     const double x = px[l], y = py[l], z = pz[l];
     double ar = 0.0, ai = 0.0;
-    for (int e = L.cou_off[T]; e < L.cou_off[T + 1]; ++e) {
+    for (int e = L.cou_off[T] + part; e < L.cou_off[T + 1]; e += L.nsplit_cou) {
         int B = L.cou_idx[e];
         if (B < L.b0 || B >= L.b1) continue;
         double cx, cy, cz;
@@ -406,7 +428,8 @@ struct CousinEv {
     double gr, gi, us, ut, up;
 };
 
-template <int PS, int PA>
+// SPLIT (small problems only, LevelParams::nsplit_cou > 1): nsplit warps per work item.
+template <int PS, int PA, bool SPLIT>
 // 5 blocks/SM (96 registers) measured best for K6
 __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const double* __restrict__ px,
                                                    const double* __restrict__ py, const double* __restrict__ pz,
@@ -417,9 +440,13 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
     constexpr int SP = P + 2;  // slot stride (double2): 4 slots -> disjoint banks for 16-byte reads
     __shared__ __align__(16) double2 sbuf[TPB / 32][2][SMAX][SP];
     __shared__ __align__(8) unsigned long long sbar[TPB / 32][2];
-    const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int nsplit = SPLIT ? L.nsplit_cou : 1;
+    const int64_t item = SPLIT ? wid / nsplit : wid;
+    const int part = SPLIT ? (int)(wid - item * nsplit) : 0;  // this warp's share of the cousin boxes
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (item >= L.nwitems) return;  // warp-uniform
+    if (SPLIT) out += (int64_t)part * (L.box_start[L.nbox]);  // field part (parts are n apart)
     if (lane == 0) {
         mbar_init(&sbar[w][0], 1);
         mbar_init(&sbar[w][1], 1);
@@ -442,10 +469,11 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
         z = pz[l];
     }
     const int e0 = L.cou_off[T], e1 = L.cou_off[T + 1];
-    auto prep = [&](int i, CousinEv<PS, PA>& v, int buf) {  // iteration i: cousin e0 + step i + half
+    const int stride = step * nsplit, cls = half + step * part;
+    auto prep = [&](int i, CousinEv<PS, PA>& v, int buf) {  // iteration i: cousin e0 + stride i + cls
         v.slot = -1;
         v.bi = -1;
-        const int e = e0 + step * i + half;
+        const int e = e0 + stride * i + cls;
         const int B = e < e1 ? L.cou_idx[e] : -1;
         if (active && B >= L.b0 && B < L.b1) {
             double cx, cy, cz;
@@ -466,7 +494,7 @@ __global__ void __launch_bounds__(128, 5) k_cousin_ws(LevelParams L, const doubl
         IFGF_DCHECK(v.bi < SMAX && v.slot < L.nseg);
     };
     double ar = 0.0, ai = 0.0;
-    const int niter = (e1 - e0 + step - 1) / step;
+    const int niter = (e1 - e0 + stride - 1) / stride;
     CousinEv<PS, PA> cur, nxt;
     if (niter > 0) prep(0, cur, 0);
     for (int i = 0; i < niter; ++i) {
@@ -1819,7 +1847,12 @@ struct Kern {
                        double2* out, int* bad) {
         if constexpr (PS > 0) {
             if (!p->legacy_cousin) {
-                k_cousin_ws<PS, PA><<<g, TPB, 0, st>>>(L, p->px, p->py, p->pz, v, p->k, out, bad, p->stage_slots);
+                if (L.nsplit_cou > 1)
+                    k_cousin_ws<PS, PA, true><<<g, TPB, 0, st>>>(L, p->px, p->py, p->pz, v, p->k, out, bad,
+                                                                 p->stage_slots);
+                else
+                    k_cousin_ws<PS, PA, false><<<g, TPB, 0, st>>>(L, p->px, p->py, p->pz, v, p->k, out, bad,
+                                                                  p->stage_slots);
                 return;
             }
         }
@@ -1944,7 +1977,7 @@ void cousin_level(ifgf_plan_s* p, int d, cudaStream_t st) {
     if (L.nseg == 0 || L.nwitems == 0) return;
     Prof pr(p, st, 4);
     const double2* vd = p->vals[d & 1];
-    dim3 g(nblk(L.nwitems * 32));
+    dim3 g(nblk(L.nwitems * L.nsplit_cou * 32));
     dispatch(
         p->Ps, p->Pa, [&] { Kern<3, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
         [&] { Kern<5, 5>::cousin(g, st, L, p, vd, p->out_sorted, p->dev_bad); },
@@ -2007,20 +2040,25 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
     const bool near = mask & IFGF_STAGE_NEAR;
     if (near) {
         Prof pr(p, sN, 1);
-        if (p->nranks > 1)  // targets without an owned neighbour get no near-field work item
-            IFGF_CUDA(cudaMemsetAsync(p->near_sorted, 0, sizeof(double2) * n, sN));
-        k_near<<<nblk(LD.p.nwitems_near * 32), TPB, 0, sN>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k,
-                                                               p->near_sorted);
+        // targets without an owned neighbour get no near-field work item (multi-rank), and
+        // with a split every part is a partial sum over its share of the neighbour boxes
+        if (p->nranks > 1 || p->nparts_near > 1)
+            IFGF_CUDA(cudaMemsetAsync(p->near_sorted, 0, sizeof(double2) * n * p->nparts_near, sN));
+        const dim3 gn(nblk(LD.p.nwitems_near * LD.p.nsplit_near * 32));
+        if (LD.p.nsplit_near > 1)
+            k_near<true><<<gn, TPB, 0, sN>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, p->near_sorted);
+        else
+            k_near<false><<<gn, TPB, 0, sN>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, p->near_sorted);
         pr.done();
         if (conc) IFGF_CUDA(cudaEventRecord(ev_near, sN));
     }
-    IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));
+    IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n * p->nparts_cou, st));
     bool have = false;        // level d holds coefficients
     bool leaf_fused = false;  // K4 fused the leaf-level fit
     if (D >= 3 && (mask & (IFGF_STAGE_COUSIN | IFGF_STAGE_UPWARD)) && LD.p.b1 > LD.p.b0) {
         if (LD.p.nseg > 0) {
             Prof pr(p, sU, 2);
-            const unsigned nb = (unsigned)(LD.p.b1 - LD.p.b0);
+            const unsigned nb = (unsigned)((LD.p.b1 - LD.p.b0) * LD.p.nsplit_s2c);
             if (LD.p.ncell <= 8 && Ps == 3 && Pa == 5) {
                 k_s2c<3, 5><<<nb, TPB, 0, sU>>>(LD.p, p->px, p->py, p->pz, p->a_sorted, p->k, Ps, Pa, p->vals[D & 1],
                                                 p->cheb_Ms, p->cheb_Ma);
@@ -2083,10 +2121,8 @@ void run_apply(ifgf_plan_s* p, const double2* dens, double2* out, cudaStream_t s
     }
     {
         Prof pr(p, st, 6);
-        if (near)
-            k_unpermute_sum<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->near_sorted, p->perm, n, out);
-        else
-            k_unpermute<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->perm, n, out);
+        k_unpermute_sum<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->nparts_cou, p->near_sorted,
+                                                      near ? p->nparts_near : 0, p->perm, n, out);
         pr.done();
     }
 }
@@ -2107,11 +2143,11 @@ void debug_level_pass(ifgf_plan_s* p, int d, const double2* values_h, unsigned w
     IFGF_CUDA(cudaMemcpyAsync(p->vals[d & 1], values_h, sizeof(double2) * (size_t)L.nseg * P, cudaMemcpyHostToDevice, st));
     fit_level(p, d, st);
     if (what & 1) {
-        IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n, st));
+        IFGF_CUDA(cudaMemsetAsync(p->out_sorted, 0, sizeof(double2) * n * p->nparts_cou, st));
         cousin_level(p, d, st);
         double2* tmp = nullptr;
         IFGF_CUDA(cudaMallocAsync((void**)&tmp, sizeof(double2) * n, st));
-        k_unpermute<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->perm, n, tmp);
+        k_unpermute_sum<<<nblk(n, 256), 256, 0, st>>>(p->out_sorted, p->nparts_cou, nullptr, 0, p->perm, n, tmp);
         IFGF_CUDA(cudaMemcpyAsync(field_h, tmp, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
         IFGF_CUDA(cudaFreeAsync(tmp, st));
     }

@@ -117,6 +117,12 @@ struct LevelParams {  // passed by value to kernels
     int up_kernel;
     int sym;  // K7 chunks grouped by quarter-turn orbits of the parent cell (reading R18)
     int cls_exact;  // 1: classify always takes the exact IEEE chain (env IFGF_EXACT_CLASSIFY; tests)
+    // source-list split of the target-major kernels on small problems: K6 (this level)
+    // and K3 (leaf level) run nsplit warps per work item, warp p taking every nsplit-th
+    // cousin / neighbour box and accumulating into field part p (summed in a fixed
+    // order by the un-permute); 1 on large problems
+    int nsplit_cou, nsplit_near;
+    int nsplit_s2c;  // K4 blocks per leaf (leaf level; small problems only)
 };
 
 constexpr int kChunk = 16;
@@ -159,8 +165,9 @@ struct ifgf_plan_s {
     double* cheb_Ma = nullptr;  // Pa x Pa
     // apply scratch
     double2* a_sorted = nullptr;
-    double2* out_sorted = nullptr;   // cousin (K6) sum, Morton order
-    double2* near_sorted = nullptr;  // near field (K3), Morton order
+    double2* out_sorted = nullptr;   // cousin (K6) sums, Morton order, nparts_cou parts of n
+    double2* near_sorted = nullptr;  // near field (K3), Morton order, nparts_near parts of n
+    int nparts_cou = 1, nparts_near = 1;
     double2* vals[2] = {nullptr, nullptr};  // ping-pong by level parity (+1 zeroed tail segment)
     double2* zseg = nullptr;                // P + 4 zeros: the TC K7's absent-column operand
     int64_t vals_cap[2] = {0, 0};

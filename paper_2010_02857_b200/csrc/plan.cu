@@ -1252,7 +1252,10 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
                     "(orbit runs %.2f), tile %.0f MB, K7 kernel %d\n",
                     d, (long long)(L.p.b1 - L.p.b0), L.p.nC, L.p.ns, (long long)ns, (long long)nrun,
                     sym ? "orbit" : "cell", per_run, per_run_orbit, tile_bytes / 1e6, kern);
-        k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, kern == 3 ? kChunkTC2 : (tc ? kChunkTC : kChunk), flag);
+        int chunk_len = kern == 3 ? kChunkTC2 : (tc ? kChunkTC : kChunk);
+        // small levels: shorter chunks, so that the pass still spans every SM (>= 2 chunks per SM)
+        if (tc) chunk_len = (int)std::min<int64_t>(chunk_len, std::max<int64_t>(16, (ns + 2 * 148 - 1) / (2 * 148)));
+        k_chunk_flag<<<nblocks(ns), TPB, 0, st>>>(rsm, ns, chunk_len, flag);
         inclusive_scan(S, flag, incl, ns, st);
         int64_t nch = d2h_one(incl + ns - 1, st);
         L.chunk_start = dev_alloc<int>(p, nch);
@@ -1268,7 +1271,7 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
             const int fs = std::max(1, L.p.ns / std::max(1, LC.ns)), fc = std::max(1, L.p.nC / std::max(1, LC.nC));
             auto nbits = [](uint64_t v) { int b = 1; while (b < 63 && ((uint64_t)1 << b) <= v) ++b; return b; };
             const int64_t tile = (int64_t)std::max(1.0, tile_bytes / std::max(1.0, child_bytes_per_box));
-            const int ch = kern == 3 ? kChunkTC2 : kChunkTC;
+            const int ch = chunk_len;
             const int bsub = nbits((uint64_t)(fs * fc * fc));
             const int bk = nbits((uint64_t)(ns / ch + 1));
             const int bcoarse = nbits((uint64_t)(L.p.ncell / (fs * fc * fc) + 1));
@@ -1343,6 +1346,28 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
         LD.p.nwitems_near = LD.p.nwitems;
     }
 
+    // 7d. source-list split of K3 / K6 on small problems: aim at >= 148 x 32 warps
+    {
+        auto split = [](int64_t nitems) {
+            const int64_t target = 148 * 32;
+            int64_t sp = nitems > 0 ? (target + nitems - 1) / nitems : 1;
+            return (int)std::max<int64_t>(1, std::min<int64_t>(8, sp));
+        };
+        p->nparts_cou = 1;
+        for (int d = 1; d <= D; ++d) {
+            LevelParams& L = p->lev[d].p;
+            L.nsplit_cou = d >= 3 ? split(L.nwitems) : 1;
+            L.nsplit_near = 1;
+            p->nparts_cou = std::max(p->nparts_cou, L.nsplit_cou);
+        }
+        p->lev[D].p.nsplit_near = split(p->lev[D].p.nwitems_near);
+        p->nparts_near = p->lev[D].p.nsplit_near;
+        for (int d = 1; d <= D; ++d) p->lev[d].p.nsplit_s2c = 1;
+        const int64_t nleaf_owned = p->lev[D].p.b1 - p->lev[D].p.b0;  // K4: >= 4 blocks per SM
+        if (nleaf_owned > 0)
+            p->lev[D].p.nsplit_s2c = (int)std::max<int64_t>(1, std::min<int64_t>(8, (4 * 148 + nleaf_owned - 1) / nleaf_owned));
+    }
+
     step_time("7c multi-rank lists");
     // 8. stats (algorithmic work units)
     {
@@ -1387,8 +1412,8 @@ void build_plan(ifgf_plan_s* p, const double* pts, const ifgf_opts& o) {
     step_time("8 stats");
     // 9. apply scratch: permuted densities, sorted field, two segment-value levels
     p->a_sorted = dev_alloc<double2>(p, n);
-    p->out_sorted = dev_alloc<double2>(p, n);
-    p->near_sorted = dev_alloc<double2>(p, n);
+    p->out_sorted = dev_alloc<double2>(p, n * p->nparts_cou);
+    p->near_sorted = dev_alloc<double2>(p, n * p->nparts_near);
     for (int par = 0; par < 2; ++par) {
         int64_t mx = 0;
         for (int d = 3; d <= D; ++d)
