@@ -1,6 +1,7 @@
 // =============================================================================
-// ifgf_oracle.cpp -- plain, serial, fp64 CPU oracle of the IFGF operator
-// evaluation (Bauinger & Bruno, arXiv 2010.02857).
+// ifgf_oracle.cpp -- plain fp64 CPU oracle of the IFGF operator evaluation
+// (Bauinger & Bruno, arXiv 2010.02857); serial, or OpenMP with bitwise the
+// serial result.
 //
 // TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
 // cpu_baseline / --impl reference legs of bench.py may load this library.
@@ -36,8 +37,11 @@
 // factorisation identity, Chebyshev node reproduction / polynomial exactness /
 // eq. 19 bound, brute-force tree relations, bypass mode == direct sum,
 // exact-recentering check, centred-source exact case, convergence in (P_s,P_ang),
-// metamorphic rotation symmetry.  Every function below is pinned by at least
-// one of those; none is "parity unpinned".
+// metamorphic rotation symmetry; the parallel mode equals the serial mode
+// bitwise, the fast classification equals the literal interval scans
+// (incl. boundary ties), and a source-partitioned plan equals the masked
+// densities exactly (tests/test_oracle_parallel.py).  Every function below is
+// pinned by at least one of those; none is "parity unpinned".
 // =============================================================================
 #include <algorithm>
 #include <cmath>
