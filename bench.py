@@ -218,7 +218,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     dfma_flops, _ = ifgf.bench_dfma(20000)  # measured FP64 FMA peak (roofline denominator)
 
-    comm = ifgf.NcclComm.from_group(None, local_rank) if world > 1 else None
+    dist_on = world > 1 or args.dist
+    comm = ifgf.NcclComm.from_group(None, local_rank) if dist_on else None
     t0 = time.perf_counter()
     plan = ifgf.Plan(pts, c.k, c.levels, c.Ps, c.Pang, rank=rank, nranks=world, comm=comm)
     torch.cuda.synchronize()
@@ -243,7 +244,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if profiled:
             plan.profile_enable(True)
             plan.profile_read(reset=True)
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -253,10 +254,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             plan.apply(a, out)
         e1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         t_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
+        if dist_on:
             dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
         return float(t_ms.item()) / args.steps
 
@@ -273,7 +274,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     out_pin = torch.empty(c.n, dtype=torch.complex128).pin_memory()
     plan.apply_host(a_pin, out_pin)  # warm
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
@@ -283,7 +284,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e3.record(stream)
     torch.cuda.synchronize()
     te = torch.tensor([e2.elapsed_time(e3)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = c.n / (float(te.item()) / args.steps * 1e-3)
 
@@ -360,6 +361,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-repeats", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="take the multi-GPU code path (process group, library NCCL communicator, in-library "
+                         "all-reduce) even with one rank: a single-GPU check of that path")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -367,15 +371,19 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
-    if world > 1:
+    if world > 1 or args.dist:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if world > 1 or args.dist:
             import torch.distributed as dist
             dist.destroy_process_group()
 
