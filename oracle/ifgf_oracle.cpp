@@ -123,11 +123,29 @@ void cheb_T(int n, double x, double* T) {
 // first-kind nodes with Lobatto weights and does not reproduce node values).
 // The interpolant at the first-kind nodes is unique; its coefficients are
 //   a_i = ((2 - delta_{i0}) / n) sum_k u(x_k) T_i(x_k).
+const int MAXP = 16;  // P_s, P_ang <= 16 (include/ifgf.h)
+
+// T_i(x_k) at the first-kind nodes of every n <= MAXP, computed once (the same
+// calls as computing them per fit, so the same bits).
+struct ChebTables {
+    double T[MAXP + 1][MAXP][MAXP];
+    ChebTables() {
+        for (int n = 1; n <= MAXP; ++n) {
+            std::vector<double> t = cheb_nodes(n);
+            for (int k = 0; k < n; ++k) cheb_T(n, t[k], T[n][k]);
+        }
+    }
+};
+const ChebTables& cheb_tables() {
+    static const ChebTables tb;  // thread-safe one-time initialisation
+    return tb;
+}
+
 void cheb_fit1d(int n, const cplx* u, cplx* a) {
-    std::vector<double> t = cheb_nodes(n), T(n);
+    const ChebTables& tb = cheb_tables();
     for (int i = 0; i < n; ++i) a[i] = 0.0;
     for (int k = 0; k < n; ++k) {
-        cheb_T(n, t[k], T.data());
+        const double* T = tb.T[n][k];
         for (int i = 0; i < n; ++i) a[i] += u[k] * T[i];
     }
     for (int i = 0; i < n; ++i) a[i] *= (i == 0 ? 1.0 : 2.0) / n;
@@ -147,31 +165,31 @@ cplx cheb_eval1d(int n, const cplx* a, double x) {
 // Nested 1-D fits along s, then theta, then phi (Theorem
 // errorestimatenested P:732-746; reading R2: order irrelevant on a tensor grid).
 void tensor_fit(int Ps, int Pa, const cplx* V, cplx* C) {
-    std::vector<cplx> A(V, V + Ps * Pa * Pa), in(std::max(Ps, Pa)), out(std::max(Ps, Pa));
+    cplx A[MAXP * MAXP * MAXP], in[MAXP], out[MAXP];
+    std::copy(V, V + Ps * Pa * Pa, A);
     for (int jp = 0; jp < Pa; ++jp)  // along s
         for (int it = 0; it < Pa; ++it) {
             for (int ks = 0; ks < Ps; ++ks) in[ks] = A[(jp * Pa + it) * Ps + ks];
-            cheb_fit1d(Ps, in.data(), out.data());
+            cheb_fit1d(Ps, in, out);
             for (int ks = 0; ks < Ps; ++ks) A[(jp * Pa + it) * Ps + ks] = out[ks];
         }
     for (int jp = 0; jp < Pa; ++jp)  // along theta
         for (int ks = 0; ks < Ps; ++ks) {
             for (int it = 0; it < Pa; ++it) in[it] = A[(jp * Pa + it) * Ps + ks];
-            cheb_fit1d(Pa, in.data(), out.data());
+            cheb_fit1d(Pa, in, out);
             for (int it = 0; it < Pa; ++it) A[(jp * Pa + it) * Ps + ks] = out[it];
         }
     for (int it = 0; it < Pa; ++it)  // along phi
         for (int ks = 0; ks < Ps; ++ks) {
             for (int jp = 0; jp < Pa; ++jp) in[jp] = A[(jp * Pa + it) * Ps + ks];
-            cheb_fit1d(Pa, in.data(), out.data());
+            cheb_fit1d(Pa, in, out);
             for (int jp = 0; jp < Pa; ++jp) A[(jp * Pa + it) * Ps + ks] = out[jp];
         }
-    std::copy(A.begin(), A.end(), C);
+    std::copy(A, A + Ps * Pa * Pa, C);
 }
 
 // Plain triple sum ("simple evaluations of triple sums"), from the
 // three 1-D Chebyshev vectors T_i(u_s), T_i(u_theta), T_i(u_phi).
-const int MAXP = 16;  // P_s, P_ang <= 16 (include/ifgf.h)
 cplx tensor_eval_T(int Ps, int Pa, const cplx* C, const double* Ts, const double* Tt, const double* Tp) {
     cplx s = 0.0;
     for (int jp = 0; jp < Pa; ++jp)
